@@ -1,0 +1,32 @@
+"""B200-native KVLinC decode hot path (arXiv 2510.05373).
+
+Drop-in replacement for the reference `quantkv` package's quantizer, cache
+and attention API (names re-exported below, as in quantkv/__init__.py:4-19),
+backed by hand-written sm_100a CUDA kernels in `libkvlinc.so` behind the C
+ABI of `include/kvlinc.h`.  There is no CPU fallback: compute calls raise on
+a host without a B200.
+
+    import paper_2510_05373_b200 as quantkv     # instead of `import quantkv`
+
+The batched serving path (B x Hkv caches, GQA decode, split-KV across GPUs)
+is `paper_2510_05373_b200.batched` / `.distributed`.
+"""
+from .adapter import (CorrectionAdapter, correction_term, feature_map, phi_k, phi_q,  # noqa: F401
+                      rng)
+from .attention import DecodePartial, decode_step_blocked  # noqa: F401
+from .cache import FootprintReport, KVCacheState, memory_footprint  # noqa: F401
+from .hadamard import HadamardMatrix, hadamard_matrix, rotate  # noqa: F401
+from .quantize import (QuantConfig, QuantizedTensor, dequantize_group,  # noqa: F401
+                       expected_quant_mse, pack_codes, quantize_group, quantize_tensor,
+                       unpack_codes)
+
+__version__ = "1.0.0"
+
+__all__ = [
+    "CorrectionAdapter", "correction_term", "feature_map", "phi_q", "phi_k", "rng",
+    "DecodePartial", "decode_step_blocked",
+    "FootprintReport", "KVCacheState", "memory_footprint",
+    "HadamardMatrix", "hadamard_matrix", "rotate",
+    "QuantConfig", "QuantizedTensor", "dequantize_group", "expected_quant_mse", "pack_codes",
+    "quantize_group", "quantize_tensor", "unpack_codes",
+]

@@ -1,0 +1,73 @@
+"""Drop-in blocked decode step (quantkv.attention.decode_step_blocked,
+attention.py:197-276) on the per-head device cache.
+
+One call = the `kvlc_ref_decode` kernel chain: phi_q / correction states,
+per-block float32 logits, max, exp, partial numerators, the ordered
+shared-max block reduction with the e^{-M}-consistent (or literal)
+correction (attention.py:158-194), the float32 H^T un-rotation and the
+divide.  Batched GQA serving decode is `batched.BatchedKVCache.decode`.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._device import empty_dev, to_dev, to_host
+from .adapter import CorrectionAdapter
+from .cache import KVCacheState
+
+
+@dataclass
+class DecodePartial:
+    """Per-block partial results of one blocked decode step (attention.py:41-47)."""
+
+    y_partial: np.ndarray   # (blocks, d) float32, in the stored value basis
+    block_max: np.ndarray   # (blocks,)
+    block_sum: np.ndarray   # (blocks,)
+
+
+def decode_step_blocked(q, cache: KVCacheState, adapter: CorrectionAdapter | None = None,
+                        block_tokens: int | None = None, literal_correction: bool = False,
+                        return_partials: bool = False):
+    """One decode step over a streamed cache, block by block (attention.py:197-276)."""
+    q = np.asarray(q, dtype=np.float64)
+    d = cache.head_dim
+    if q.shape != (d,):
+        raise ValueError(f"query shape {q.shape} != head dim ({d},)")
+    if cache.tokens_total == 0:
+        raise ValueError("cannot decode against an empty cache")
+    block = cache.group_size if block_tokens is None else block_tokens
+    if block < 1:
+        raise ValueError(f"block_tokens must be >= 1, got {block}")
+
+    st = cache._storage()
+    use_adapter = (adapter is not None and adapter.enabled and st["s"] is not None)
+    rank = cache.adapter_rank if use_adapter else 0
+    if use_adapter:
+        w1q, w2q, _, _ = adapter.device_weights()
+    nq, nr = cache.quantized_tokens, cache.residual_len
+    nb = -(-nq // block) + (1 if nr else 0)
+    lib = _lib.load()
+    scratch = empty_dev((lib.kvlc_ref_decode_scratch(d, nq, nr, block, rank),), "u8")
+    d_out = empty_dev((d,), "f64")
+    py = empty_dev((max(nb, 1), d), "f32") if return_partials else None
+    pm = empty_dev((max(nb, 1),), "f32") if return_partials else None
+    pl = empty_dev((max(nb, 1),), "f32") if return_partials else None
+    n_chunks = cache._n_chunks
+    d_q = to_dev(q)
+    _lib.call("kvlc_ref_decode", _lib.ptr(d_q), d, cache.group_size, cache.config_k.bits,
+              int(cache.values_rotated), n_chunks,
+              _lib.ptr(st["kwords"]), _lib.ptr(st["kscales"]), _lib.ptr(st["kzeros"]),
+              _lib.ptr(st["vwords"]), _lib.ptr(st["vscales"]), _lib.ptr(st["vzeros"]),
+              nr, _lib.ptr(st["res_k"]), _lib.ptr(st["res_v"]),
+              _lib.ptr(w1q) if use_adapter else None, _lib.ptr(w2q) if use_adapter else None,
+              _lib.ptr(st["s"]) if use_adapter else None, _lib.ptr(st["p"]) if use_adapter else None,
+              rank, block, int(bool(literal_correction)), _lib.ptr(d_out),
+              _lib.ptr(py), _lib.ptr(pm), _lib.ptr(pl), _lib.ptr(scratch), _lib.stream_handle())
+    out = to_host(d_out, "f64")
+    if return_partials:
+        return out, DecodePartial(y_partial=to_host(py[:nb], "f32"), block_max=to_host(pm[:nb], "f32"),
+                                  block_sum=to_host(pl[:nb], "f32"))
+    return out

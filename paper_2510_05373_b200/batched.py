@@ -1,0 +1,284 @@
+"""Batched serving API: a [B, Hkv] 2-bit KVLinC cache on one B200.
+
+Shapes are fixed at the production configuration the fast kernels
+specialise on: head_dim d = 128, group G = 128, residual window R = 128,
+adapter rank D = 256, 2-bit codes; GQA groups of 1..8 query heads per KV
+head.  Activations (q, k, v, out) are bf16; scales / zeros are fp16 (the
+.kvlc on-disk precision, cache.py:220-224); S / P are fp32.
+
+    cache = BatchedKVCache(batch=16, kv_heads=8, q_heads=32, max_tokens=8192)
+    bank = AdapterBank.initialize(kv_heads=8)          # one adapter per kv head
+    cache.prefill(k, v, adapters=bank)                 # k, v: [B, Hkv, N, 128] bf16
+    out = cache.decode(q, adapters=bank)               # q: [B, Hq, 128] bf16
+    cache.append(k_t, v_t, adapters=bank)              # one token per sequence
+
+Per (b, kv-head) the semantics are those of the reference's KVCacheState +
+decode_step_blocked (cache.py:120-158, attention.py:197-276) with
+query head h reading kv head h // (Hq // Hkv).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import D, G, R, RANK, SLOTS, KvlcAdapter, KvlcCache, KvlcDecodeOpts
+from .adapter import CorrectionAdapter
+
+REC_FLOATS = 4 + 2 * D      # device-partial record: m_log2, l, 0, 0, y_rot[D], y_raw[D]
+CORR_FLOATS = 1 + D         # correction record: C_d, C_n[D]
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class AdapterBank:
+    """One CorrectionAdapter per kv head, fp32 device weights [Hkv][128][128]."""
+
+    def __init__(self, adapters, enabled: bool = True, device=None):
+        _lib.require_device()
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        for ad in adapters:
+            if ad.head_dim != D or ad.rank != RANK:
+                raise ValueError(f"serving adapters must be d={D}, rank={RANK}; got "
+                                 f"d={ad.head_dim}, rank={ad.rank}")
+        stack = lambda name: torch.from_numpy(np.stack([getattr(a, name) for a in adapters])
+                                              .astype(np.float32)).to(dev).contiguous()
+        self.adapters = list(adapters)
+        self.w1q, self.w2q = stack("w1_q"), stack("w2_q")
+        self.w1k, self.w2k = stack("w1_k"), stack("w2_k")
+        self.enabled = enabled and all(a.enabled for a in adapters)
+
+    @classmethod
+    def initialize(cls, kv_heads: int, seeds=None, init_scale: float = 1.0, device=None):
+        """Random-init adapters, seed = kv-head index by default."""
+        seeds = list(range(kv_heads)) if seeds is None else list(seeds)
+        return cls([CorrectionAdapter.initialize(D, RANK, seed=s, init_scale=init_scale)
+                    for s in seeds], device=device)
+
+    def struct(self) -> KvlcAdapter:
+        return KvlcAdapter(self.w1q.data_ptr(), self.w2q.data_ptr(), self.w1k.data_ptr(),
+                           self.w2k.data_ptr(), int(self.enabled))
+
+
+def flush_count(lens, keep_window: bool = True) -> np.ndarray:
+    """Chunks flushed after `lens` streaming appends: floor((len - R) / G) for
+    len >= R (the flush fires when the window holds R + G tokens,
+    cache.py:129), or floor(len / G) when no window is kept."""
+    lens = np.asarray(lens, np.int64)
+    if keep_window:
+        return np.where(lens >= R, (lens - R) // G, 0)
+    return lens // G
+
+
+def _adapter_struct(adapters):
+    if adapters is None:
+        return KvlcAdapter(None, None, None, None, 0)
+    return adapters.struct()
+
+
+class BatchedKVCache:
+    """Device-resident [B, Hkv] KVLinC cache (layout: include/kvlinc.h `kvlc_cache`)."""
+
+    def __init__(self, batch: int, kv_heads: int, q_heads: int, max_tokens: int, device=None):
+        _lib.require_device()
+        if q_heads % kv_heads or q_heads // kv_heads > 8:
+            raise ValueError(f"q_heads {q_heads} must be a multiple of kv_heads {kv_heads} "
+                             "with at most 8 query heads per kv head")
+        if batch > 1024:
+            raise ValueError("batch must be <= 1024")
+        self.B, self.Hkv, self.Hq = batch, kv_heads, q_heads
+        self.group = q_heads // kv_heads
+        self.max_tokens = max_tokens
+        self.max_chunks = max(1, -(-max(0, max_tokens - R) // G))
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        U, C = batch * kv_heads, self.max_chunks
+        z = lambda shape, dt: torch.zeros(shape, dtype=dt, device=dev)
+        self.kcodes = z((U, C, 8, 128), torch.int32)
+        self.vcodes = z((U, C, 8, 128), torch.int32)
+        self.kscale = z((U, C, 128), torch.float16)
+        self.kzero = z((U, C, 128), torch.float16)
+        self.vscale = z((U, C, 128), torch.float16)
+        self.vzero = z((U, C, 128), torch.float16)
+        self.kres = z((U, SLOTS, D), torch.bfloat16)
+        self.vres = z((U, D, SLOTS), torch.bfloat16)
+        self.S = z((U, D, RANK), torch.float32)
+        self.P = z((U, RANK), torch.float32)
+        self.n_chunks_dev = z((batch,), torch.int32)
+        self.res_start_dev = z((batch,), torch.int32)
+        self.res_len_dev = z((batch,), torch.int32)
+        # host mirror of the per-sequence counters (the host drives flushes)
+        self.n_chunks = np.zeros(batch, np.int64)
+        self.res_start = np.zeros(batch, np.int64)
+        self.res_len = np.zeros(batch, np.int64)
+        self._ws = None
+        self._struct = self._make_struct()
+
+    # ------------------------------------------------------------------ plumbing
+    def _make_struct(self) -> KvlcCache:
+        p = lambda t: t.data_ptr()
+        return KvlcCache(self.B, self.Hkv, self.Hq, self.max_chunks, p(self.kcodes), p(self.vcodes),
+                         p(self.kscale), p(self.kzero), p(self.vscale), p(self.vzero), p(self.kres),
+                         p(self.vres), p(self.S), p(self.P), p(self.n_chunks_dev),
+                         p(self.res_start_dev), p(self.res_len_dev))
+
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    @property
+    def tokens(self) -> np.ndarray:
+        return self.n_chunks * G + self.res_len
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in
+                   (self.kcodes, self.vcodes, self.kscale, self.kzero, self.vscale, self.vzero,
+                    self.kres, self.vres, self.S, self.P))
+
+    # ------------------------------------------------------------------ writers
+    def prefill(self, k: torch.Tensor, v: torch.Tensor, lens=None, adapters: AdapterBank | None = None,
+                keep_window: bool = True):
+        """Load N tokens per sequence (== N streaming appends, cache.py:120-130).
+
+        k, v: bf16 [B, Hkv, N, 128] (device or host).  lens: per-sequence
+        token counts (default N).  keep_window=False flushes every whole
+        chunk (a non-tail shard of a sequence-parallel cache, see
+        `distributed`).  The cache must be empty."""
+        if np.any(self.tokens):
+            raise ValueError("prefill needs an empty cache")
+        if k.shape != v.shape or k.dim() != 4 or k.shape[:2] != (self.B, self.Hkv) or k.shape[3] != D:
+            raise ValueError(f"token dims {tuple(k.shape)}/{tuple(v.shape)} != ({self.B}, {self.Hkv}, n, {D})")
+        n = k.shape[2]
+        lens = np.full(self.B, n, np.int32) if lens is None else np.asarray(lens, np.int32)
+        k = k.to(self.device, torch.bfloat16).contiguous()
+        v = v.to(self.device, torch.bfloat16).contiguous()
+        lib = _lib.load()
+        ws = self.workspace(lib.kvlc_prefill_workspace(ctypes.byref(self._struct), n))
+        ad = _adapter_struct(adapters)
+        lens_c = (ctypes.c_int32 * self.B)(*lens.tolist())
+        _lib.call("kvlc_prefill", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(k), _ptr(v), n,
+                  lens_c, int(bool(keep_window)), _ptr(ws), ws.numel(), _lib.stream_handle())
+        nf = flush_count(lens, keep_window)
+        self.n_chunks[:] = nf
+        self.res_start[:] = 0
+        self.res_len[:] = lens - nf * G
+
+    def append(self, k_t: torch.Tensor, v_t: torch.Tensor, adapters: AdapterBank | None = None,
+               active=None):
+        """Append one token per (active) sequence: k_t, v_t bf16 [B, Hkv, 128].
+        A sequence whose window reaches R + G flushes its oldest G tokens."""
+        if k_t.shape != (self.B, self.Hkv, D) or v_t.shape != k_t.shape:
+            raise ValueError(f"token dims {tuple(k_t.shape)}/{tuple(v_t.shape)} != ({self.B}, {self.Hkv}, {D})")
+        act = np.ones(self.B, bool) if active is None else np.asarray(active, bool)
+        new_len = self.res_len + act
+        flush = act & (new_len == R + G)
+        if np.any(self.n_chunks + flush > self.max_chunks):
+            raise ValueError(f"append exceeds capacity of {self.max_tokens} tokens")
+        ad = _adapter_struct(adapters)
+        a_c = (ctypes.c_int32 * self.B)(*act.astype(np.int32).tolist())
+        f_c = (ctypes.c_int32 * self.B)(*flush.astype(np.int32).tolist())
+        k_t = k_t.to(self.device, torch.bfloat16).contiguous()
+        v_t = v_t.to(self.device, torch.bfloat16).contiguous()
+        _lib.call("kvlc_append", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
+                  a_c, f_c, None, 0, _lib.stream_handle())
+        self.res_len = new_len - flush * G
+        self.res_start = np.where(flush, (self.res_start + G) % SLOTS, self.res_start)
+        self.n_chunks = self.n_chunks + flush
+
+    # ------------------------------------------------------------------ decode
+    def _opts(self, literal=False, chunks_per_split=0, out_fp32=False) -> KvlcDecodeOpts:
+        return KvlcDecodeOpts(int(chunks_per_split), int(bool(literal)), int(self.n_chunks.max()),
+                              int(bool(out_fp32)))
+
+    def decode_workspace_bytes(self, literal=False, chunks_per_split=0) -> int:
+        o = self._opts(literal, chunks_per_split)
+        return _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
+
+    def decode(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False,
+               out: torch.Tensor | None = None, chunks_per_split: int = 0,
+               out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+        """Fused GQA decode step: q bf16 [B, Hq, 128] -> out [B, Hq, 128] (bf16, or
+        float32 with out_dtype=torch.float32)."""
+        if q.shape != (self.B, self.Hq, D):
+            raise ValueError(f"query shape {tuple(q.shape)} != ({self.B}, {self.Hq}, {D})")
+        if np.any(self.tokens == 0):
+            raise ValueError("cannot decode against an empty cache")
+        q = q.to(self.device, torch.bfloat16).contiguous()
+        if out is None:
+            out = torch.empty(q.shape, dtype=out_dtype, device=self.device)
+        if out.dtype not in (torch.bfloat16, torch.float32) or out.shape != q.shape:
+            raise ValueError("out must be a [B, Hq, 128] bf16 or float32 tensor")
+        o = self._opts(literal, chunks_per_split, out.dtype == torch.float32)
+        nbytes = _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
+        ws = self.workspace(nbytes)
+        ad = _adapter_struct(adapters)
+        _lib.call("kvlc_decode", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(q), _ptr(out),
+                  ctypes.byref(o), _ptr(ws), ws.numel(), _lib.stream_handle())
+        return out
+
+    def decode_partial(self, q: torch.Tensor, chunk_lo: int, chunk_hi: int, include_tail: bool,
+                       adapters: AdapterBank | None = None, chunks_per_split: int = 0,
+                       rec: torch.Tensor | None = None, corr: torch.Tensor | None = None):
+        """Partial decode over quantized chunks [chunk_lo, chunk_hi) (+ the residual
+        window and the correction when include_tail): returns (rec, corr) with
+        rec fp32 [B, Hq, 4 + 2*128] = (m_log2, l, 0, 0, y_rot, y_raw) and corr fp32
+        [B, Hq, 1 + 128] = (C_d, C_n) (zeros unless include_tail)."""
+        q = q.to(self.device, torch.bfloat16).contiguous()
+        if rec is None:
+            rec = torch.empty((self.B, self.Hq, REC_FLOATS), dtype=torch.float32, device=self.device)
+        if corr is None:
+            corr = torch.zeros((self.B, self.Hq, CORR_FLOATS), dtype=torch.float32, device=self.device)
+        o = self._opts(False, chunks_per_split)
+        nbytes = _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
+        ws = self.workspace(nbytes)
+        ad = _adapter_struct(adapters)
+        _lib.call("kvlc_decode_partial", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(q),
+                  int(chunk_lo), int(chunk_hi), int(bool(include_tail)), _ptr(rec),
+                  _ptr(corr) if include_tail else None, ctypes.byref(o), _ptr(ws), ws.numel(),
+                  _lib.stream_handle())
+        return rec, corr
+
+    # ------------------------------------------------------------------ export
+    def export_chunk(self, b: int, kvh: int, chunk: int) -> dict:
+        """One quantized chunk in the reference layout (channel-axis key words
+        (8, 128), value_rows words (128, 8), fp16 metadata)."""
+        u = b * self.Hkv + kvh
+        dev = self.device
+        kw = torch.empty((8, 128), dtype=torch.int32, device=dev)
+        vw = torch.empty((128, 8), dtype=torch.int32, device=dev)
+        meta = torch.empty((4, 128), dtype=torch.float16, device=dev)
+        _lib.call("kvlc_export_chunk", ctypes.byref(self._struct), u, chunk, _ptr(kw), _ptr(vw),
+                  _ptr(meta[0]), _ptr(meta[1]), _ptr(meta[2]), _ptr(meta[3]), _lib.stream_handle())
+        m = meta.cpu().numpy()
+        return dict(kwords=kw.cpu().numpy().view(np.uint32), vwords=vw.cpu().numpy().view(np.uint32),
+                    kscale=m[0], kzero=m[1], vscale=m[2], vzero=m[3])
+
+    def residual(self, b: int, kvh: int):
+        """Live residual window of one unit, oldest first, as float32 host arrays."""
+        u = b * self.Hkv + kvh
+        start, n = int(self.res_start[b]), int(self.res_len[b])
+        slots = [(start + i) % SLOTS for i in range(n)]
+        k = self.kres[u].float().cpu().numpy()[slots]
+        v = self.vres[u].float().cpu().numpy()[:, slots].T
+        return k, v
+
+
+def merge_records(recs: torch.Tensor, corr: torch.Tensor | None, literal: bool = False,
+                  out: torch.Tensor | None = None, out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+    """LSE-merge n records [n, B, Hq, 4 + 2*128] (+ correction [B, Hq, 129])
+    into out bf16 [B, Hq, 128] (`kvlc_merge_records`)."""
+    n, B, Hq, width = recs.shape
+    if width != REC_FLOATS:
+        raise ValueError(f"record width {width} != {REC_FLOATS}")
+    recs = recs.contiguous()
+    if out is None:
+        out = torch.empty((B, Hq, D), dtype=out_dtype, device=recs.device)
+    _lib.call("kvlc_merge_records", _ptr(recs), n, B * Hq * REC_FLOATS,
+              _ptr(corr.contiguous()) if corr is not None else None, B, Hq, int(bool(literal)),
+              int(out.dtype == torch.float32), _ptr(out), _lib.stream_handle())
+    return out

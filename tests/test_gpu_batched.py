@@ -1,0 +1,220 @@
+"""Batched serving path (fused flush + split-KV GQA decode) vs the CPU oracle.
+
+Numerics contract:
+  T1 packed code words, chunk / residual counters: bit-exact
+  T2 fp16 scale / zero: exactly float16(reference float64 value)
+  T3 S, P: relative Frobenius <= 1e-5 against the float64 reference states
+  T4 decode output vs decode_step_blocked on the fp16-metadata oracle cache:
+     max-abs <= 1e-3 * max|ref|
+  T5 correction isolation: (out_adapter - out_plain) within 5% relative
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import kvlinc_oracle as orc  # noqa: E402
+from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache, merge_records  # noqa: E402
+from kvlc_testutil import bf16_round  # noqa: E402
+
+D = 128
+F32 = torch.float32
+
+
+def make_inputs(B, Hkv, Hq, n, seed=0):
+    g = orc.rng(seed)
+    k = bf16_round(g.standard_normal((B, Hkv, n, D)).astype(np.float32))
+    v = bf16_round(g.standard_normal((B, Hkv, n, D)).astype(np.float32))
+    q = bf16_round(g.standard_normal((B, Hq, D)).astype(np.float32))
+    return k, v, q
+
+
+def tdev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda().to(torch.bfloat16)
+
+
+def oracle_caches(k, v, lens, adapters):
+    B, Hkv = k.shape[:2]
+    return [[orc.build_cache(k[b, h, :lens[b]], v[b, h, :lens[b]],
+                             adapters[h] if adapters else None) for h in range(Hkv)] for b in range(B)]
+
+
+def check_cache_exact(cache, ocs, lens):
+    B, Hkv = len(ocs), len(ocs[0])
+    for b in range(B):
+        oc0 = ocs[b][0]
+        assert cache.n_chunks[b] == len(oc0.key_chunks)
+        assert cache.res_len[b] == oc0.residual_len
+        for h in range(Hkv):
+            oc = ocs[b][h]
+            for ci, ch in enumerate(oc.key_chunks):
+                ex = cache.export_chunk(b, h, ci)
+                assert np.array_equal(ex["kwords"], ch.words), (b, h, ci)
+                assert np.array_equal(ex["kscale"], ch.scales[0].astype(np.float16)), (b, h, ci)
+                assert np.array_equal(ex["kzero"], ch.zeros[0].astype(np.float16)), (b, h, ci)
+                sl = slice(ci * 128, (ci + 1) * 128)
+                assert np.array_equal(ex["vwords"], oc.value_words[sl]), (b, h, ci)
+                assert np.array_equal(ex["vscale"], oc.value_scales[sl, 0].astype(np.float16)), (b, h, ci)
+                assert np.array_equal(ex["vzero"], oc.value_zeros[sl, 0].astype(np.float16)), (b, h, ci)
+            rk, rv = cache.residual(b, h)
+            assert np.array_equal(rk, oc.residual_keys().astype(np.float32))
+            assert np.array_equal(rv, oc.residual_values().astype(np.float32))
+
+
+def check_states(cache, ocs):
+    for b in range(len(ocs)):
+        for h in range(len(ocs[0])):
+            oc = ocs[b][h]
+            u = b * cache.Hkv + h
+            S = cache.S[u].double().cpu().numpy()
+            P = cache.P[u].double().cpu().numpy()
+            if oc.s_state is None:
+                assert not S.any() and not P.any()
+                continue
+            assert np.linalg.norm(S - oc.s_state) <= 1e-5 * np.linalg.norm(oc.s_state), (b, h)
+            assert np.linalg.norm(P - oc.p_state) <= 1e-5 * np.linalg.norm(oc.p_state), (b, h)
+
+
+def oracle_decode(q, ocs, adapters, literal=False):
+    B, Hq, _ = q.shape
+    g = Hq // len(ocs[0])
+    out = np.zeros((B, Hq, D))
+    for b in range(B):
+        for h in range(Hq):
+            oc = orc.fp16_meta_copy(ocs[b][h // g])
+            out[b, h] = orc.decode_blocked(q[b, h], oc, adapters[h // g] if adapters else None,
+                                           literal=literal)
+    return out
+
+
+@pytest.mark.parametrize("Hkv,Hq,lens", [(2, 8, [900, 511]), (1, 7, [640]), (2, 2, [300, 1000]),
+                                         (1, 8, [385])])
+def test_prefill_and_decode_vs_oracle(Hkv, Hq, lens):
+    B = len(lens)
+    n = max(lens)
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=Hq * 10 + B)
+    oads = [orc.init_adapter(D, 256, seed=h) for h in range(Hkv)]
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k), tdev(v), lens=lens, adapters=bank)
+    ocs = oracle_caches(k, v, lens, oads)
+    check_cache_exact(cache, ocs, lens)
+    check_states(cache, ocs)
+    for literal in (False, True):
+        out = cache.decode(tdev(q), adapters=bank, literal=literal, out_dtype=F32).cpu().numpy()
+        ref = oracle_decode(q, ocs, oads, literal=literal)
+        err = np.abs(out - ref).max()
+        assert err <= 1e-3 * np.abs(ref).max(), (literal, err, np.abs(ref).max())
+    plain = cache.decode(tdev(q), out_dtype=F32).cpu().numpy()
+    ref_plain = oracle_decode(q, ocs, None)
+    assert np.abs(plain - ref_plain).max() <= 1e-3 * np.abs(ref_plain).max()
+    ref_ad = oracle_decode(q, ocs, oads)
+    out_ad = cache.decode(tdev(q), adapters=bank, out_dtype=F32).cpu().numpy()
+    delta_ref, delta = ref_ad - ref_plain, out_ad - plain
+    if np.abs(delta_ref).max() > 0:
+        assert np.abs(delta - delta_ref).max() <= 0.05 * np.abs(delta_ref).max() + 2e-3 * np.abs(ref_ad).max()
+
+
+def test_append_stream_crosses_flushes():
+    B, Hkv, Hq = 2, 2, 8
+    lens0 = [250, 100]
+    steps = 300
+    n = max(lens0) + steps
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=7)
+    oads = [orc.init_adapter(D, 256, seed=h) for h in range(Hkv)]
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k[:, :, :max(lens0)]), tdev(v[:, :, :max(lens0)]), lens=lens0, adapters=bank)
+    pos = list(lens0)
+    for s in range(steps):
+        kt = np.stack([k[b, :, pos[b]] for b in range(B)])
+        vt = np.stack([v[b, :, pos[b]] for b in range(B)])
+        cache.append(tdev(kt), tdev(vt), adapters=bank)
+        pos = [p + 1 for p in pos]
+    lens = pos
+    ocs = oracle_caches(k, v, lens, oads)
+    check_cache_exact(cache, ocs, lens)
+    check_states(cache, ocs)
+    out = cache.decode(tdev(q), adapters=bank, out_dtype=F32).cpu().numpy()
+    ref = oracle_decode(q, ocs, oads)
+    assert np.abs(out - ref).max() <= 1e-3 * np.abs(ref).max()
+
+
+def test_split_partials_merge_equals_full_decode():
+    B, Hkv, Hq, n = 2, 2, 8, 1500
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=3)
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k), tdev(v), lens=[n, n - 333], adapters=bank)
+    qd = tdev(q)
+    full = cache.decode(qd, adapters=bank, out_dtype=F32)
+    nch = int(cache.n_chunks.max())
+    for parts in (2, 3, 4):
+        bounds = np.linspace(0, nch, parts + 1).astype(int)
+        recs, corr = [], None
+        for i in range(parts):
+            tail = i == parts - 1
+            rec, c = cache.decode_partial(qd, int(bounds[i]), int(bounds[i + 1]), tail, adapters=bank)
+            recs.append(rec)
+            if tail:
+                corr = c
+        merged = merge_records(torch.stack(recs), corr, out_dtype=F32)
+        assert (merged - full).abs().max().item() <= 1e-5 * full.abs().max().item()
+        for literal in (True,):
+            m2 = merge_records(torch.stack(recs), corr, literal=literal, out_dtype=F32)
+            f2 = cache.decode(qd, adapters=bank, literal=literal, out_dtype=F32)
+            assert (m2 - f2).abs().max().item() <= 1e-5 * f2.abs().max().item()
+
+
+def test_correction_dominated_extremes():
+    # all-ones keys, q = +-300: exp terms underflow and out ~ H^T C_n / C_d
+    B, Hkv, Hq, n = 1, 1, 4, 700
+    g = orc.rng(15)
+    k = np.ones((B, Hkv, n, D))
+    v = bf16_round(g.standard_normal((B, Hkv, n, D)).astype(np.float32))
+    oads = [orc.init_adapter(D, 256, seed=0)]
+    bank = AdapterBank.initialize(1)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k), tdev(v), adapters=bank)
+    ocs = oracle_caches(k, v, [n], oads)
+    for sign in (300.0, -300.0):
+        q = np.full((B, Hq, D), sign)
+        out = cache.decode(tdev(q), adapters=bank, out_dtype=F32).cpu().numpy()
+        assert np.all(np.isfinite(out))
+        ref = oracle_decode(q, ocs, oads)
+        assert np.abs(out - ref).max() <= 1e-2 * max(1e-6, np.abs(ref).max())
+
+
+def test_short_and_empty_windows():
+    B, Hkv, Hq = 3, 1, 4
+    lens = [1, 128, 255]  # residual only, exactly the window, window + G - 1
+    n = max(lens)
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=11)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=512)
+    cache.prefill(tdev(k), tdev(v), lens=lens)
+    assert list(cache.n_chunks) == [0, 0, 0]
+    ocs = oracle_caches(k, v, lens, None)
+    out = cache.decode(tdev(q), out_dtype=F32).cpu().numpy()
+    ref = oracle_decode(q, ocs, None)
+    assert np.abs(out - ref).max() <= 1e-3 * np.abs(ref).max()
+    with pytest.raises(ValueError, match="empty cache"):
+        BatchedKVCache(1, 1, 4, max_tokens=256).decode(tdev(q[:1]))
+
+
+def test_value_tie_tokens_match_reference_codes():
+    """n=4096 / seed 4100 holds a genuine (x-min)/scale = 0.5 +- 1ulp value tie
+    (chunk 14, token 39, channel 17).  The serving flush re-evaluates such
+    tokens in the reference's arithmetic order, so every code matches."""
+    g = orc.rng(4100)
+    n = 4096
+    k = bf16_round(g.standard_normal((1, 1, n, D)).astype(np.float32))
+    v = bf16_round(g.standard_normal((1, 1, n, D)).astype(np.float32))
+    q = bf16_round(g.standard_normal((1, 4, D)).astype(np.float32))
+    cache = BatchedKVCache(1, 1, 4, max_tokens=n + 256)
+    cache.prefill(tdev(k), tdev(v))
+    ocs = oracle_caches(k, v, [n], None)
+    check_cache_exact(cache, ocs, [n])
+    out = cache.decode(tdev(q), out_dtype=F32).cpu().numpy()
+    ref = oracle_decode(q, ocs, None)
+    assert np.abs(out - ref).max() <= 1e-3 * np.abs(ref).max()
