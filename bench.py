@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py — fused 2-bit KVLinC decode attention on B200 (BASELINE.json metric).
+
+Workload (BASELINE config 2, the headline): Llama-3-8B attention shapes,
+batch 16 per GPU, 32 q / 8 kv heads, d = 128, context 8192, 2-bit KVLinC cache
+(G = R = 128, D = 256 random-init adapter per kv head), synthetic bf16 data.
+A step = one fused decode (Algorithm 1) for every (sequence, q-head):
+phi_q prologue + split-KV kernel + LSE combine.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one rank per GPU: every rank decodes its own
+batch-16 shard ((b, kv-head) units are independent — no collective on the
+data path), timed with CUDA events, max over ranks; value = tokens/s of the
+whole job (weak scaling).
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port, oracle/kvlinc_oracle.py — the reference is pure NumPy) on all
+host cores of rank 0, same metric / config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("decode-attn µs/step & HBM GB/s vs roofline; speedup vs bf16 FlashAttn decode")
+B, HKV, HQ, CTX, D, G, R, RANK = 16, 8, 32, 8192, 128, 128, 128, 256
+REPLICAS = 4   # rotating caches: 4 x 101 MB > 126 MB L2, every step streams from HBM
+
+
+def algo_bytes_split(b, hkv, hq, nq, nr):
+    """Algorithmic bytes the split-KV kernel must move: packed K/V
+    codes, fp16 scale/zero, bf16 residual window, fp32 S, bf16 q, fp32 phi."""
+    g = hq // hkv
+    per_unit = (2 * nq * D // 4 + (nq // G) * D * 4 + nq * 4 + nr * D * 4 + D * RANK * 4
+                + g * D * 2 + g * RANK * 4)
+    return b * hkv * per_unit
+
+
+def algo_bytes_step(b, hkv, hq, nq, nr):
+    """Whole decode step: + P, q/out bf16 per unit, W1q/W2q per kv head."""
+    g = hq // hkv
+    per_unit = (2 * nq * D // 4 + (nq // G) * D * 4 + nq * 4 + nr * D * 4 + D * RANK * 4 + RANK * 4
+                + g * D * 2 * 2)
+    return b * hkv * per_unit + hkv * 2 * D * (RANK // 2) * 4
+
+
+def workload_config(world):
+    return {"workload": "llama3-8b-shapes fused 2-bit KVLinC decode (BASELINE config 2)",
+            "batch_per_gpu": B, "global_batch": B * world, "q_heads": HQ, "kv_heads": HKV,
+            "head_dim": D, "ctx": CTX, "bits": 2, "group": G, "residual_window": R,
+            "adapter_rank": RANK, "parallelism": f"dp{world} over (b, kv-head) units",
+            "l2": f"{REPLICAS} rotating cache replicas ({REPLICAS} x 101 MB > 126 MB L2)"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except OSError:
+            return None
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        if not sm:
+            return None
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, val in zip(names, r[5:9]):
+                if val.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache, flush_count
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    torch.manual_seed(1234 + rank)
+    bank = AdapterBank.initialize(HKV, device=dev)
+    caches = []
+    for _ in range(REPLICAS):
+        c = BatchedKVCache(B, HKV, HQ, CTX + 256, device=dev)
+        k = torch.randn(B, HKV, CTX, D, device=dev).bfloat16()
+        v = torch.randn(B, HKV, CTX, D, device=dev).bfloat16()
+        c.prefill(k, v, adapters=bank)
+        del k, v
+        caches.append(c)
+    torch.cuda.synchronize()
+    nq = int(flush_count([CTX])[0]) * G
+    nr = CTX - nq
+    q = torch.randn(B, HQ, D, device=dev).bfloat16()
+    out = torch.empty_like(q)
+    K, W = args.steps, args.warmup
+    evb = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    eve = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    for e in evb + eve:   # materialise the CUDA events before handing them to the C ABI
+        e.record()
+    torch.cuda.synchronize()
+    for i in range(W):
+        caches[i % REPLICAS].decode(q, adapters=bank, out=out)
+    torch.cuda.synchronize()
+    # one CUDA graph per replica: the step's three PDL-chained kernels in one launch
+    graphs = [c.capture_decode(q, adapters=bank, out=out)[0] for c in caches]
+    for i in range(W):
+        graphs[i % REPLICAS].replay()
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region (inputs resident in HBM) ----
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t0.record()
+        for i in range(K):
+            graphs[i % REPLICAS].replay()
+        t1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = t0.elapsed_time(t1) / K
+
+    # ---- the dominant kernel alone: events recorded on its stream around each launch ----
+    for i in range(K):
+        caches[i % REPLICAS].decode(q, adapters=bank, out=out, events=(evb[i], eve[i]))
+    torch.cuda.synchronize()
+    split_ms = sum(evb[i].elapsed_time(eve[i]) for i in range(K)) / K
+
+    # ---- end-to-end through the public API: pinned host q in, host out back, every step ----
+    q_host = torch.empty((B, HQ, D), dtype=torch.bfloat16).pin_memory()
+    q_host.copy_(q.cpu())
+    out_host = torch.empty((B, HQ, D), dtype=torch.bfloat16).pin_memory()
+    for i in range(W):
+        q.copy_(q_host, non_blocking=True)
+        graphs[i % REPLICAS].replay()
+        out_host.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(K):
+        q.copy_(q_host, non_blocking=True)
+        graphs[i % REPLICAS].replay()
+        out_host.copy_(out, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / K
+
+    times = torch.tensor([step_ms, split_ms, e2e_ms], device=dev)
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    step_ms, split_ms, e2e_ms = (float(x) for x in times.tolist())
+    if rank != 0:
+        return None
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    split_bytes = algo_bytes_split(B, HKV, HQ, nq, nr)
+    step_bytes = algo_bytes_step(B, HKV, HQ, nq, nr)
+    achieved = split_bytes / (split_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "split_kernel_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+
+    result = {
+        "metric": METRIC, "value": B * world / (step_ms * 1e-3), "unit": "tokens/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 activations / 2-bit codes / fp16 meta / fp32 accumulate",
+        "data": "synthetic N(0,1) bf16 K/V/q, random-init adapters (seed = kv head)",
+        "config": workload_config(world),
+        "us_per_step": step_ms * 1e3,
+        "hbm_gbs_step": step_bytes / (step_ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
+                     "frac": achieved / peak_gbs, "traffic": traffic,
+                     "kernel": "split_kernel (kvlc_decode.cu)", "split_us": split_ms * 1e3,
+                     "algorithmic_bytes_per_launch": split_bytes,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+        "step_roofline_frac": step_bytes / (step_ms * 1e-3) / 1e9 / peak_gbs,
+        "e2e": {"value": B * world / (e2e_ms * 1e-3), "unit": "tokens/s",
+                "h2d_bytes_per_step": B * HQ * D * 2, "d2h_bytes_per_step": B * HQ * D * 2,
+                "ms_per_step": e2e_ms},
+        "gpu_launches": 3 * K,
+        "launch": "CUDA graph per step (phi_kernel -> split_kernel -> combine_kernel, PDL-chained)",
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_fa:
+        result["bf16_flash_attn"] = run_flash_attn(args, dev, step_ms)
+    if world == 1 and not args.no_cpu:
+        result["cpu_baseline"] = cpu_baseline_sample()
+    return result
+
+
+def run_flash_attn(args, dev, ours_ms):
+    """bf16 FlashAttention-2 decode (flash_attn_with_kvcache) on the same shapes."""
+    import torch
+    try:
+        from flash_attn import flash_attn_with_kvcache
+    except Exception as e:  # pragma: no cover
+        return {"unavailable": str(e)}
+    kc = torch.randn(B, CTX, HKV, D, device=dev).bfloat16()
+    vc = torch.randn(B, CTX, HKV, D, device=dev).bfloat16()
+    q = torch.randn(B, 1, HQ, D, device=dev).bfloat16()
+    lens = torch.full((B,), CTX, dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        flash_attn_with_kvcache(q, kc, vc, cache_seqlens=lens)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        flash_attn_with_kvcache(q, kc, vc, cache_seqlens=lens)
+    e1.record()
+    torch.cuda.synchronize()
+    fa_ms = e0.elapsed_time(e1) / args.steps
+    fa_bytes = 2 * B * CTX * HKV * D * 2 + 2 * B * HQ * D * 2
+    return {"impl": "flash_attn 2.8.3 flash_attn_with_kvcache (bf16 KV)", "us_per_step": fa_ms * 1e3,
+            "hbm_gbs": fa_bytes / (fa_ms * 1e-3) / 1e9, "speedup_ours_vs_fa": fa_ms / ours_ms}
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def _oracle_unit_worker(args):
+    """One (b, kv-head) unit of the workload on one core: build its cache with the
+    oracle's streaming rule, then time decode_step_blocked for its g q-heads."""
+    kvh, reps, seed = args
+    from threadpoolctl import threadpool_limits
+    import numpy as np
+    from oracle import kvlinc_oracle as orc
+    with threadpool_limits(1):
+        g = orc.rng(seed)
+        k = g.standard_normal((CTX, D)).astype(np.float32).astype(np.float64)
+        v = g.standard_normal((CTX, D)).astype(np.float32).astype(np.float64)
+        ad = orc.init_adapter(D, RANK, seed=kvh)
+        cache = orc.build_cache(k, v, ad)
+        qs = g.standard_normal((HQ // HKV, D))
+        times = []
+        for _ in range(reps):
+            t = time.perf_counter()
+            for h in range(HQ // HKV):
+                orc.decode_blocked(qs[h], cache, ad)
+            times.append(time.perf_counter() - t)
+        return times
+
+
+def cpu_baseline_sample():
+    """Single-core sample: one kv unit (4 q-heads) of the workload, extrapolated
+    to the full step (B*Hkv = 128 units)."""
+    t_unit = statistics.median(_oracle_unit_worker((0, 3, 7)))
+    step_s = t_unit * B * HKV
+    return {"value": B / step_s, "unit": "tokens/s", "cores": 1, "kind": "port",
+            "sample": f"1 of {B * HKV} (b, kv-head) units, {HQ // HKV} q-heads, ctx {CTX}, "
+                      f"oracle decode_step_blocked (O(N) value slicing), median of 3; "
+                      f"{t_unit * 1e3:.1f} ms per unit, extrapolated x{B * HKV}",
+            "ms_per_step": step_s * 1e3}
+
+
+def run_reference(args, world):
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    K, W = args.steps, args.warmup
+    with mp.get_context("fork").Pool(cores) as pool:
+        # each worker owns one unit; a step's sample = `cores` units decoded in parallel
+        res = pool.map(_oracle_unit_worker, [(i % HKV, K + W, 100 + i) for i in range(cores)])
+    per_round = [max(r[i] for r in res) for i in range(W, W + K)]   # wall time of one round
+    rounds = -(-B * HKV // cores)
+    step_s = statistics.mean(per_round) * rounds
+    value = B / step_s
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": step_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "float64 host / float32 block arithmetic (reference semantics)",
+            "data": "synthetic N(0,1) K/V/q, random-init adapters",
+            "config": workload_config(1),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": f"each step: {cores} of {B * HKV} (b, kv-head) units decoded "
+                                       f"in parallel (1 per core), x{rounds} rounds extrapolated"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-fa", action="store_true", help="skip the bf16 FlashAttention comparison")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle sample")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args, world)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    result = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

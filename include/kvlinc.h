@@ -208,6 +208,8 @@ typedef struct kvlc_decode_opts {
   int32_t literal;
   int32_t max_chunks_hint; /* max n_chunks over the batch (host mirror) */
   int32_t out_fp32;        /* 1: `out` is float32 [B][Hq][128] instead of bf16 */
+  void* ev_begin;          /* optional cudaEvent_t recorded right before / after */
+  void* ev_end;            /* the split-KV kernel (measurement hook, may be NULL) */
 } kvlc_decode_opts;
 
 /* Fused GQA decode (Algorithm 1 / decode_step_blocked, attention.py:197-276)

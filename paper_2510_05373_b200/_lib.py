@@ -38,7 +38,7 @@ class KvlcAdapter(ctypes.Structure):
 class KvlcDecodeOpts(ctypes.Structure):
     """Mirror of `kvlc_decode_opts`."""
     _fields_ = [("chunks_per_split", c_int32), ("literal", c_int32), ("max_chunks_hint", c_int32),
-                ("out_fp32", c_int32)]
+                ("out_fp32", c_int32), ("ev_begin", c_void_p), ("ev_end", c_void_p)]
 
 
 class KvlcError(RuntimeError):

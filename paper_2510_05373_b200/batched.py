@@ -191,9 +191,10 @@ class BatchedKVCache:
         self.n_chunks = self.n_chunks + flush
 
     # ------------------------------------------------------------------ decode
-    def _opts(self, literal=False, chunks_per_split=0, out_fp32=False) -> KvlcDecodeOpts:
+    def _opts(self, literal=False, chunks_per_split=0, out_fp32=False, events=None) -> KvlcDecodeOpts:
+        ev0, ev1 = (events[0].cuda_event, events[1].cuda_event) if events else (None, None)
         return KvlcDecodeOpts(int(chunks_per_split), int(bool(literal)), int(self.n_chunks.max()),
-                              int(bool(out_fp32)))
+                              int(bool(out_fp32)), ev0, ev1)
 
     def decode_workspace_bytes(self, literal=False, chunks_per_split=0) -> int:
         o = self._opts(literal, chunks_per_split)
@@ -201,9 +202,10 @@ class BatchedKVCache:
 
     def decode(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False,
                out: torch.Tensor | None = None, chunks_per_split: int = 0,
-               out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+               out_dtype: torch.dtype = torch.bfloat16, events=None) -> torch.Tensor:
         """Fused GQA decode step: q bf16 [B, Hq, 128] -> out [B, Hq, 128] (bf16, or
-        float32 with out_dtype=torch.float32)."""
+        float32 with out_dtype=torch.float32).  events=(begin, end) torch.cuda.Event
+        pair recorded around the split-KV kernel (measurement hook)."""
         if q.shape != (self.B, self.Hq, D):
             raise ValueError(f"query shape {tuple(q.shape)} != ({self.B}, {self.Hq}, {D})")
         if np.any(self.tokens == 0):
@@ -213,13 +215,27 @@ class BatchedKVCache:
             out = torch.empty(q.shape, dtype=out_dtype, device=self.device)
         if out.dtype not in (torch.bfloat16, torch.float32) or out.shape != q.shape:
             raise ValueError("out must be a [B, Hq, 128] bf16 or float32 tensor")
-        o = self._opts(literal, chunks_per_split, out.dtype == torch.float32)
+        o = self._opts(literal, chunks_per_split, out.dtype == torch.float32, events)
         nbytes = _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
         ws = self.workspace(nbytes)
         ad = _adapter_struct(adapters)
         _lib.call("kvlc_decode", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(q), _ptr(out),
                   ctypes.byref(o), _ptr(ws), ws.numel(), _lib.stream_handle())
         return out
+
+    def capture_decode(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False,
+                       out: torch.Tensor | None = None, chunks_per_split: int = 0):
+        """Capture one decode step on fixed q / out buffers into a CUDA graph
+        (the three PDL-chained launches replay with one graph launch).
+        Returns (graph, out); refill q in place and call graph.replay()."""
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.bfloat16, device=self.device)
+        self.decode(q, adapters, literal, out, chunks_per_split)   # sizes the workspace
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            self.decode(q, adapters, literal, out, chunks_per_split)
+        return graph, out
 
     def decode_partial(self, q: torch.Tensor, chunk_lo: int, chunk_hi: int, include_tail: bool,
                        adapters: AdapterBank | None = None, chunks_per_split: int = 0,

@@ -106,7 +106,7 @@ struct DecArgs {
   float* corr;            // [B][Hq][1 + D]  (C_d, C_n)
   float* rec;             // [U][nrec][NG][REC]
   int nsq;                // quantized split CTAs per unit
-  int cpw;                // chunks per warp
+  int cpc;                // chunks per quantized-split CTA
   int chunk_lo, chunk_hi; // global chunk window (split-KV across devices)
   int tail;               // include residual window + correction rows
   int corr_on;            // adapter active
@@ -114,402 +114,90 @@ struct DecArgs {
 };
 
 // ---------------------------------------------------------------- phi_q ----
-template <int NG>
-__global__ void __launch_bounds__(256) phi_kernel(kvlc_cache c, const float* __restrict__ w1q,
+// One CTA per (kv head, block of PHI_QB queries of that kv head): the queries
+// of all sequences that share W1q/W2q are batched, so each W column is read
+// once per block (coalesced across the 256 feature threads).
+constexpr int PHI_QB = 8;
+
+__global__ void __launch_bounds__(256) phi_kernel(kvlc_cache c, int NG, const float* __restrict__ w1q,
                                                   const float* __restrict__ w2q,
                                                   const uint16_t* __restrict__ q,
                                                   float* __restrict__ phi, float* __restrict__ corr) {
   griddep_launch();
-  __shared__ float qs[NG][D];
-  __shared__ float red[8][NG];
-  __shared__ float stat[2][NG];
-  const int unit = blockIdx.x, b = unit / c.Hkv, kvh = unit % c.Hkv;
+  __shared__ float qs[PHI_QB][D];
+  __shared__ float red[8][PHI_QB];
+  __shared__ float stat[2][PHI_QB];
+  const int kvh = blockIdx.x, j0 = blockIdx.y * PHI_QB, nj = c.B * NG;
   const int f = threadIdx.x, warp = f >> 5, lane = f & 31, half = f >> 7;
-  const size_t qbase = ((size_t)b * c.Hq + (size_t)kvh * NG) * D;
-  for (int i = f; i < NG * D; i += 256) qs[i / D][i % D] = bf2f(q[qbase + i]);
+  // query j of this kv head = (b = j / NG, head kvh*NG + j % NG)
+  auto qrow = [&](int j) { return (size_t)(j / NG) * c.Hq + (size_t)kvh * NG + j % NG; };
+  for (int i = f; i < PHI_QB * D; i += 256) {
+    const int j = j0 + i / D;
+    qs[i / D][i % D] = j < nj ? bf2f(q[qrow(j) * D + i % D]) : 0.f;
+  }
   __syncthreads();
   const float* W = (half ? w2q : w1q) + (size_t)kvh * D * HALF + (f & (HALF - 1));
-  float acc[NG];
+  float acc[PHI_QB];
 #pragma unroll
-  for (int i = 0; i < NG; ++i) acc[i] = 0.f;
+  for (int i = 0; i < PHI_QB; ++i) acc[i] = 0.f;
+#pragma unroll 8
   for (int ch = 0; ch < D; ++ch) {
-    float w = __ldg(W + ch * HALF);
+    const float w = __ldg(W + ch * HALF);
 #pragma unroll
-    for (int i = 0; i < NG; ++i) acc[i] = fmaf(qs[i][ch], w, acc[i]);
+    for (int i = 0; i < PHI_QB; ++i) acc[i] = fmaf(qs[i][ch], w, acc[i]);
   }
   // max-shifted softmax within each half (linalg.py:38-47)
 #pragma unroll
-  for (int i = 0; i < NG; ++i) {
-    float m = warp_max(acc[i]);
+  for (int i = 0; i < PHI_QB; ++i) {
+    const float m = warp_max(acc[i]);
     if (lane == 0) red[warp][i] = m;
   }
   __syncthreads();
-  if (f < 2 * NG) {
-    int h = f / NG, i = f % NG;
-    float m = red[4 * h][i];
-    for (int w = 1; w < 4; ++w) m = fmaxf(m, red[4 * h + w][i]);
-    stat[h][i] = m;
+  if (f < 2 * PHI_QB) {
+    const int h = f / PHI_QB, i = f % PHI_QB;
+    stat[h][i] = fmaxf(fmaxf(red[4 * h][i], red[4 * h + 1][i]), fmaxf(red[4 * h + 2][i], red[4 * h + 3][i]));
   }
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < NG; ++i) acc[i] = expf(acc[i] - stat[half][i]);
+  for (int i = 0; i < PHI_QB; ++i) acc[i] = expf(acc[i] - stat[half][i]);
 #pragma unroll
-  for (int i = 0; i < NG; ++i) {
-    float s = warp_sum(acc[i]);
+  for (int i = 0; i < PHI_QB; ++i) {
+    const float s = warp_sum(acc[i]);
     if (lane == 0) red[warp][i] = s;
   }
   __syncthreads();
-  if (f < 2 * NG) {
-    int h = f / NG, i = f % NG;
-    float s = 0.f;
-    for (int w = 0; w < 4; ++w) s += red[4 * h + w][i];
-    stat[h][i] = s;
-  }
-  __syncthreads();
-  const float pf = c.P[(size_t)unit * RANK + f];
-#pragma unroll
-  for (int i = 0; i < NG; ++i) {
-    float ph = acc[i] / stat[half][i];
-    phi[(qbase / D + i) * RANK + f] = ph;
-    acc[i] = pf * ph;
+  if (f < 2 * PHI_QB) {
+    const int h = f / PHI_QB, i = f % PHI_QB;
+    stat[h][i] = (red[4 * h][i] + red[4 * h + 1][i]) + (red[4 * h + 2][i] + red[4 * h + 3][i]);
   }
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < NG; ++i) {
-    float s = warp_sum(acc[i]);
+  for (int i = 0; i < PHI_QB; ++i) {
+    const int j = j0 + i;
+    const float ph = acc[i] / stat[half][i];
+    float cd = 0.f;
+    if (j < nj) {
+      phi[qrow(j) * RANK + f] = ph;
+      cd = c.P[((size_t)(j / NG) * c.Hkv + kvh) * RANK + f] * ph;
+    }
+    acc[i] = cd;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < PHI_QB; ++i) {
+    const float s = warp_sum(acc[i]);
     if (lane == 0) red[warp][i] = s;
   }
   __syncthreads();
-  if (f < NG) {
+  if (f < PHI_QB && j0 + f < nj) {
     float s = 0.f;
+#pragma unroll
     for (int w = 0; w < 8; ++w) s += red[w][f];
-    corr[(qbase / D + f) * (1 + D)] = s;  // C_d
+    corr[qrow(j0 + f) * (1 + D)] = s;  // C_d = P . phi_q
   }
 }
 
-// ------------------------------------------------------ per-warp state ----
-// Heads handled per thread in the C layout: HILO -> head t; else heads 2t, 2t+1.
-template <int NG>
-struct WarpState {
-  static constexpr bool HILO = NG <= 4;
-  static constexpr int NH = HILO ? 1 : 2;
-  float m[NH], l[NH], z[NH];
-  float acc[8][4];
-  __device__ __forceinline__ void init() {
-#pragma unroll
-    for (int e = 0; e < NH; ++e) {
-      m[e] = -INFINITY;
-      l[e] = 0.f;
-      z[e] = 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  }
-};
-
-// One quantized chunk (128 tokens) for one warp.
-// EXTRA (groups of > 4 heads only): bit 0 adds a low-part pass to Q K^T,
-// bit 1 adds a low-part pass to P V (hi + lo fp16 operands, two MMAs).
-template <int NG, int EXTRA>
-__device__ __forceinline__ void quant_chunk(const kvlc_cache& c, size_t cb, const uint32_t (&qh)[8][2],
-                                            WarpState<NG>& st, int lane) {
-  constexpr bool HILO = NG <= 4;
-  constexpr bool QK_LO = !HILO && (EXTRA & 1);
-  constexpr bool PV_LO = !HILO && (EXTRA & 2);
-  const int g = lane >> 2, t = lane & 3;
-  // ---- loads: K words (word row g, channels 16kt+4t..+3), K meta, V words (row g, slots 16i+4t..) ----
-  uint4 kw[8], vw[8];
-  uint2 ks[8], kz[8];
-  const uint32_t* kc = c.kcodes + (cb * 8 + g) * 128 + 4 * t;
-  const uint32_t* vc = c.vcodes + (cb * 8 + g) * 128 + 4 * t;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) kw[i] = ldg4(kc + 16 * i);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    ks[i] = ldg2(c.kscale + cb * D + 16 * i + 4 * t);
-    kz[i] = ldg2(c.kzero + cb * D + 16 * i + 4 * t);
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) vw[i] = ldg4(vc + 16 * i);
-  const uint4 vs0 = ldg4(c.vscale + cb * G + 16 * g), vs1 = ldg4(c.vscale + cb * G + 16 * g + 8);
-  const uint4 vz0 = ldg4(c.vzero + cb * G + 16 * g), vz1 = ldg4(c.vzero + cb * G + 16 * g + 8);
-
-  // ---- B operand for QK: q' = q * s_k (hi / lo fp16), and zt = q . z_k ----
-  uint32_t bq[8][2];
-  uint32_t bql[QK_LO ? 8 : 1][2];
-  float zp = 0.f;
-  const __half2 lo_mask = (HILO && (g & 1)) ? u2h(0xffffffffu) : u2h(0u);
-#pragma unroll
-  for (int kt = 0; kt < 8; ++kt) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      __half2 qv = u2h(qh[kt][e]);
-      __half2 sv = u2h(e ? ks[kt].y : ks[kt].x);
-      __half2 hi = __hmul2(qv, sv);
-      if (HILO) {
-        // odd columns carry the low part q*s - hi (exact FMA residual)
-        uint32_t neg = (h2u(hi) ^ 0x80008000u) & h2u(lo_mask);
-        __half2 r = __hfma2(qv, sv, u2h(neg));
-        bq[kt][e] = h2u(r);
-      } else {
-        bq[kt][e] = h2u(hi);
-        if (QK_LO) bql[kt][e] = h2u(__hfma2(qv, sv, __hneg2(hi)));
-      }
-      float2 qf = __half22float2(qv);
-      float2 zf = __half22float2(u2h(e ? kz[kt].y : kz[kt].x));
-      zp = fmaf(qf.x, zf.x, zp);
-      zp = fmaf(qf.y, zf.y, zp);
-    }
-  }
-  zp += __shfl_xor_sync(0xffffffffu, zp, 1);
-  zp += __shfl_xor_sync(0xffffffffu, zp, 2);
-  float zt[WarpState<NG>::NH];
-  if (HILO) {
-    zt[0] = __shfl_sync(0xffffffffu, zp, 8 * t) * C0;
-  } else {
-    zt[0] = __shfl_sync(0xffffffffu, zp, 8 * t) * C0;
-    zt[1] = __shfl_sync(0xffffffffu, zp, 8 * t + 4) * C0;
-  }
-
-  // ---- QK^T: 8 token tiles x 8 channel tiles ----
-  float cq[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) cq[i][j] = 0.f;
-#pragma unroll
-  for (int kt = 0; kt < 8; ++kt) {
-#pragma unroll
-    for (int bb = 0; bb < 4; ++bb) {
-      uint32_t x0 = pick(kw[kt].x, kw[kt].y, bb), x1 = pick(kw[kt].z, kw[kt].w, bb);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int mt = 2 * bb + h;
-        mma_f16(cq[mt], code_h2(x0, 2 * h), code_h2(x0, 2 * h + 1), code_h2(x1, 2 * h),
-                code_h2(x1, 2 * h + 1), bq[kt][0], bq[kt][1]);
-        if (QK_LO)
-          mma_f16(cq[mt], code_h2(x0, 2 * h), code_h2(x0, 2 * h + 1), code_h2(x1, 2 * h),
-                  code_h2(x1, 2 * h + 1), bql[QK_LO ? kt : 0][0], bql[QK_LO ? kt : 0][1]);
-      }
-    }
-  }
-
-  // ---- online softmax over this chunk (tokens 16g + 2mt + r) ----
-  constexpr int NH = WarpState<NG>::NH;
-  float cmax[NH];
-#pragma unroll
-  for (int e = 0; e < NH; ++e) cmax[e] = -INFINITY;
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const float F = code_unscale(2 * (mt & 1) + r) * C0;
-      if (HILO) {
-        float v = fmaf(cq[mt][2 * r] + cq[mt][2 * r + 1], F, zt[0]);
-        cq[mt][2 * r] = v;
-        cmax[0] = fmaxf(cmax[0], v);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          float v = fmaf(cq[mt][2 * r + e], F, zt[e]);
-          cq[mt][2 * r + e] = v;
-          cmax[e] = fmaxf(cmax[e], v);
-        }
-      }
-    }
-  }
-  float sc[NH];
-#pragma unroll
-  for (int e = 0; e < NH; ++e) {
-    float m = cmax[e];
-    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
-    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
-    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
-    float mn = fmaxf(st.m[e], m);
-    sc[e] = exp2f(st.m[e] - mn);
-    st.m[e] = mn;
-    st.l[e] *= sc[e];
-    st.z[e] *= sc[e];
-  }
-#pragma unroll
-  for (int mv = 0; mv < 8; ++mv) {
-    if (HILO) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) st.acc[mv][j] *= sc[0];
-    } else {
-      st.acc[mv][0] *= sc[0];
-      st.acc[mv][2] *= sc[0];
-      st.acc[mv][1] *= sc[1];
-      st.acc[mv][3] *= sc[1];
-    }
-  }
-  // p, l, z and the PV B operand p' = p * s_v (hi/lo or two heads), transposed by movmatrix
-  uint32_t bp[8][2];
-  uint32_t bpl[PV_LO ? 8 : 1][2];
-  const uint32_t vsw[8] = {vs0.x, vs0.y, vs0.z, vs0.w, vs1.x, vs1.y, vs1.z, vs1.w};
-  const uint32_t vzw[8] = {vz0.x, vz0.y, vz0.z, vz0.w, vz1.x, vz1.y, vz1.z, vz1.w};
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    const float2 s2 = __half22float2(u2h(vsw[mt]));  // tokens 2mt, 2mt+1
-    const float2 z2 = __half22float2(u2h(vzw[mt]));
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const float sv = r ? s2.y : s2.x, zv = r ? z2.y : z2.x;
-      uint32_t packed;
-      if (HILO) {
-        float p = exp2f(cq[mt][2 * r] - st.m[0]);
-        st.l[0] += p;
-        st.z[0] = fmaf(p, zv, st.z[0]);
-        float pv = p * sv;
-        __half hi = __float2half_rn(pv);
-        __half lo = __float2half_rn(pv - __half2float(hi));
-        packed = h2u(__halves2half2(hi, lo));
-      } else {
-        float p0 = exp2f(cq[mt][2 * r] - st.m[0]);
-        float p1 = exp2f(cq[mt][2 * r + 1] - st.m[1]);
-        st.l[0] += p0;
-        st.l[1] += p1;
-        st.z[0] = fmaf(p0, zv, st.z[0]);
-        st.z[1] = fmaf(p1, zv, st.z[1]);
-        const float a0 = p0 * sv, a1 = p1 * sv;
-        const __half2 hh = __floats2half2_rn(a0, a1);
-        packed = h2u(hh);
-        if (PV_LO) {
-          const float2 hf = __half22float2(hh);
-          bpl[PV_LO ? mt : 0][r] = movm_t(h2u(__floats2half2_rn(a0 - hf.x, a1 - hf.y)));
-        }
-      }
-      bp[mt][r] = movm_t(packed);
-    }
-  }
-
-  // ---- P V: 8 channel tiles x 8 token tiles ----
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    const int i0 = mt >> 1, ln = 2 * (mt & 1);
-#pragma unroll
-    for (int bb = 0; bb < 4; ++bb) {
-      uint32_t x0 = pick(w4(vw[i0], ln), w4(vw[4 + i0], ln), bb);
-      uint32_t x1 = pick(w4(vw[i0], ln + 1), w4(vw[4 + i0], ln + 1), bb);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int mv = 2 * bb + h;
-        mma_f16(st.acc[mv], code_h2(x0, 2 * h), code_h2(x0, 2 * h + 1), code_h2(x1, 2 * h),
-                code_h2(x1, 2 * h + 1), bp[mt][0], bp[mt][1]);
-        if (PV_LO)
-          mma_f16(st.acc[mv], code_h2(x0, 2 * h), code_h2(x0, 2 * h + 1), code_h2(x1, 2 * h),
-                  code_h2(x1, 2 * h + 1), bpl[PV_LO ? mt : 0][0], bpl[PV_LO ? mt : 0][1]);
-      }
-    }
-  }
-}
-
-// Writes this warp's (m, l, y[c]) per head into shared memory.
-// Quantized layout: channel 16g + 2mv + r with factor 2^24 4^-(2(mv&1)+r);
-// residual layout: channel 16mv + g + 8r, no factor.
-template <int NG, bool QUANT>
-__device__ __forceinline__ void warp_store(WarpState<NG>& st, float* smrec, int lane) {
-  constexpr bool HILO = NG <= 4;
-  constexpr int NH = WarpState<NG>::NH;
-  const int g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int e = 0; e < NH; ++e) {
-    float l = st.l[e], z = st.z[e];
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      l += __shfl_xor_sync(0xffffffffu, l, o);
-      z += __shfl_xor_sync(0xffffffffu, z, o);
-    }
-    st.l[e] = l;
-    st.z[e] = z;
-  }
-#pragma unroll
-  for (int e = 0; e < NH; ++e) {
-    const int h = HILO ? t : 2 * t + e;
-    if (h >= NG) continue;
-    float* r = smrec + h * REC;
-    if (g == 0) {
-      r[0] = st.m[e];
-      r[1] = st.l[e];
-    }
-#pragma unroll
-    for (int mv = 0; mv < 8; ++mv) {
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        float v = HILO ? st.acc[mv][2 * rr] + st.acc[mv][2 * rr + 1] : st.acc[mv][2 * rr + e];
-        int ch;
-        if (QUANT) {
-          v = fmaf(v, code_unscale(2 * (mv & 1) + rr), st.z[e]);
-          ch = 16 * g + 2 * mv + rr;
-        } else {
-          ch = 16 * mv + g + 8 * rr;
-        }
-        r[4 + ch] = v;
-      }
-    }
-  }
-}
-
-// Merges the WARPS per-warp records in shared memory into one global record per head.
-template <int NG>
-__device__ __forceinline__ void cta_merge(const float* sm, float* out) {
-  for (int i = threadIdx.x; i < NG * REC; i += THREADS) {
-    const int h = i / REC, k = i % REC;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) M = fmaxf(M, sm[(w * NG + h) * REC]);
-    float v;
-    if (k == 0) {
-      v = M;
-    } else {
-      v = 0.f;
-      if (M != -INFINITY) {
-#pragma unroll
-        for (int w = 0; w < WARPS; ++w) {
-          float mw = sm[(w * NG + h) * REC];
-          if (mw != -INFINITY) v = fmaf(exp2f(mw - M), sm[(w * NG + h) * REC + k], v);
-        }
-      }
-    }
-    out[h * REC + k] = v;
-  }
-}
-
-template <int NG, int EXTRA>
-__device__ void run_quant(const DecArgs& a, int unit, int split, float* smrec) {
-  const kvlc_cache& c = a.c;
-  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  constexpr bool HILO = NG <= 4;
-  // q fragments (fp16) for B column n = g
-  uint32_t qh[8][2];
-  {
-    const int head = HILO ? (g >> 1) : g;
-    const bool valid = head < NG;
-    const uint16_t* qp = a.q + ((size_t)b * c.Hq + (size_t)kvh * NG + (valid ? head : 0)) * D + 4 * t;
-#pragma unroll
-    for (int kt = 0; kt < 8; ++kt) {
-      uint2 raw = valid ? ldg2(qp + 16 * kt) : make_uint2(0u, 0u);
-      float f0 = __uint_as_float(raw.x << 16), f1 = __uint_as_float(raw.x & 0xffff0000u);
-      float f2 = __uint_as_float(raw.y << 16), f3 = __uint_as_float(raw.y & 0xffff0000u);
-      qh[kt][0] = h2u(__floats2half2_rn(f0, f1));
-      qh[kt][1] = h2u(__floats2half2_rn(f2, f3));
-    }
-  }
-  WarpState<NG> st;
-  st.init();
-  const int n_ch = min(c.n_chunks[b], a.chunk_hi);
-  const int lo = a.chunk_lo + split * a.cpw * WARPS;
-  const int hi = min(n_ch, lo + a.cpw * WARPS);
-  for (int ci = lo + warp; ci < hi; ci += WARPS)
-    quant_chunk<NG, EXTRA>(c, (size_t)unit * c.max_chunks + ci, qh, st, lane);
-  warp_store<NG, true>(st, smrec + warp * NG * REC, lane);
-  __syncthreads();
-  cta_merge<NG>(smrec, a.rec + ((size_t)unit * a.nrec + split) * NG * REC);
-}
+#include "kvlc_quant.cuh"
 
 // Residual window half hf: ring slots [128 hf, 128 hf + 128), 32 per warp.
 __device__ __forceinline__ int res_sigma(int r) {  // QK row -> slot offset within a 16-slot tile
@@ -588,6 +276,7 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
       m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
       st.m[e] = m;  // finite: at least one live slot in the warp
+      st.mt[e] = m;
     }
     uint32_t bhi[2][2], blo[2][2];
 #pragma unroll
@@ -655,6 +344,13 @@ __device__ void run_corr(const DecArgs& a, int unit, int rb) {
     sr[r][0] = __ldg(sp);
     sr[r][1] = __ldg(sp + 1);
   }
+  // per-lane partial dots for the warp's 8 rows x NG heads, then one
+  // reduce-scatter per 32 values: lane L ends with the total of value L
+  constexpr int NV = (CORR_ROWS / WARPS) * NG;
+  constexpr int NB = (NV + 31) / 32;
+  float vals[NB * 32];
+#pragma unroll
+  for (int n = 0; n < NB * 32; ++n) vals[n] = 0.f;
 #pragma unroll
   for (int r = 0; r < CORR_ROWS / WARPS; ++r) {
     const float s8[8] = {sr[r][0].x, sr[r][0].y, sr[r][0].z, sr[r][0].w,
@@ -664,19 +360,38 @@ __device__ void run_corr(const DecArgs& a, int unit, int rb) {
       float v = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) v = fmaf(s8[k], ph[i][k], v);
-      v = warp_sum(v);
-      if (lane == i) a.corr[(qh0 + i) * (1 + D) + 1 + row0 + r] = v;
+      vals[r * NG + i] = v;
+    }
+  }
+#pragma unroll
+  for (int blk = 0; blk < NB; ++blk) {
+    float* x = vals + 32 * blk;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool upper = lane & s;
+#pragma unroll
+      for (int k = 0; k < s; ++k) {
+        const float send = upper ? x[k] : x[k + s];
+        const float keep = upper ? x[k + s] : x[k];
+        x[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+    }
+    const int n = 32 * blk + lane;
+    if (n < NV) {
+      const int r = n / NG, i = n % NG;
+      a.corr[(qh0 + i) * (1 + D) + 1 + row0 + r] = x[0];
     }
   }
 }
 
 template <int NG, int EXTRA>
-__global__ void __launch_bounds__(THREADS, 2) split_kernel(const DecArgs a) {
-  __shared__ __align__(16) float smrec[WARPS * NG * REC];
+__global__ void __launch_bounds__(THREADS, 4) split_kernel(const DecArgs a) {
+  __shared__ __align__(16) SplitSmem sm;
+  float* smrec = sm.rec;
   const int U = a.c.B * a.c.Hkv;
   int x = blockIdx.x;
   if (x < U * a.nsq) {
-    run_quant<NG, EXTRA>(a, x / a.nsq, x % a.nsq, smrec);
+    run_quant<NG, EXTRA>(a, x / a.nsq, x % a.nsq, sm);
     return;
   }
   x -= U * a.nsq;
@@ -721,7 +436,13 @@ struct CombArgs {
 };
 
 // Shared tail: apply the correction rule and produce out = (H num_rot + num_raw)/den.
-__device__ __forceinline__ void finish(float M, float den, float (&nr)[4], float (&nw)[4],
+// num/den are expressed in the frame 2^-M (M = max of the records' reference
+// points); Mt is the true global logit max (the reference's M, attention.py:172-175).
+// Consistent correction: C enters as the m = 0 partial, i.e. scaled by 2^-M when
+// M >= 0, else the blocks are scaled by 2^M (attention.py:190-194); both are the
+// same value as the reference's e^-M_true form.  Literal mode adds C unscaled in
+// the true-max frame (attention.py:188-189).
+__device__ __forceinline__ void finish(float M, float Mt, float den, float (&nr)[4], float (&nw)[4],
                                        const float* corr, int literal, int lane, void* out,
                                        int out_fp32) {
   if (corr) {
@@ -733,9 +454,13 @@ __device__ __forceinline__ void finish(float M, float den, float (&nr)[4], float
     any = __any_sync(0xffffffffu, any);
     if (any) {
       if (literal) {
+        const float s = M == -INFINITY ? 0.f : exp2f(M - Mt);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) nr[e] += cn[e];
-        den += cd;
+        for (int e = 0; e < 4; ++e) {
+          nr[e] = fmaf(s, nr[e], cn[e]);
+          nw[e] *= s;
+        }
+        den = fmaf(s, den, cd);
       } else if (M >= 0.f) {
         const float s = exp2f(-M);
 #pragma unroll
@@ -773,34 +498,59 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombArgs a) {
   const int b = gw / a.Hq, qh = gw % a.Hq, kvh = qh / a.NG, h = qh % a.NG;
   const int unit = b * a.Hkv + kvh;
   const float* base = a.rec + (size_t)unit * a.nrec * a.NG * REC + (size_t)h * REC;
-  float M = -INFINITY;
-  for (int r = 0; r < a.nrec; ++r) M = fmaxf(M, base[(size_t)r * a.NG * REC]);
+  const size_t rstride = (size_t)a.NG * REC;
+  // lanes hold the records' (m, l); weights via one warp max / sum, then the
+  // numerators stream with independent loads.
+  float M = -INFINITY, Mt = -INFINITY;
+  for (int r0 = 0; r0 < a.nrec; r0 += 32) {
+    const int r = r0 + lane;
+    if (r < a.nrec) {
+      M = fmaxf(M, base[r * rstride]);
+      Mt = fmaxf(Mt, base[r * rstride + 2]);
+    }
+  }
+  M = warp_max(M);
+  Mt = warp_max(Mt);
   float nr[4] = {0.f, 0.f, 0.f, 0.f}, nw[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
   if (M != -INFINITY) {
-    for (int r = 0; r < a.nrec; ++r) {
-      const float* rr = base + (size_t)r * a.NG * REC;
-      const float m = rr[0];
-      if (m == -INFINITY) continue;
-      const float w = exp2f(m - M);
-      den = fmaf(w, rr[1], den);
-      const float4 y = *reinterpret_cast<const float4*>(rr + 4 + 4 * lane);
-      float* dst = r < a.nsq ? nr : nw;
-      dst[0] = fmaf(w, y.x, dst[0]);
-      dst[1] = fmaf(w, y.y, dst[1]);
-      dst[2] = fmaf(w, y.z, dst[2]);
-      dst[3] = fmaf(w, y.w, dst[3]);
+    for (int r0 = 0; r0 < a.nrec; r0 += 32) {
+      const int r = r0 + lane, cnt = min(32, a.nrec - r0);
+      float w = 0.f;
+      if (r < a.nrec) {
+        const float m = base[r * rstride];
+        w = m == -INFINITY ? 0.f : exp2f(m - M);
+        den = fmaf(w, base[r * rstride + 1], den);
+      }
+#pragma unroll 4
+      for (int i = 0; i < cnt; ++i) {
+        const float wi = __shfl_sync(0xffffffffu, w, i);
+        const float4 y = *reinterpret_cast<const float4*>(base + (r0 + i) * rstride + 4 + 4 * lane);
+        if (r0 + i < a.nsq) {  // warp-uniform: quantized (rotated) vs residual (raw) basis
+          nr[0] = fmaf(wi, y.x, nr[0]);
+          nr[1] = fmaf(wi, y.y, nr[1]);
+          nr[2] = fmaf(wi, y.z, nr[2]);
+          nr[3] = fmaf(wi, y.w, nr[3]);
+        } else {
+          nw[0] = fmaf(wi, y.x, nw[0]);
+          nw[1] = fmaf(wi, y.y, nw[1]);
+          nw[2] = fmaf(wi, y.z, nw[2]);
+          nw[3] = fmaf(wi, y.w, nw[3]);
+        }
+      }
     }
+    den = warp_sum(den);
   }
   if (a.rec_out) {  // partial mode: (M, den, num_rot, num_raw), no correction
     float* o = a.rec_out + (size_t)gw * PREC;
-    if (lane == 0) *reinterpret_cast<float4*>(o) = make_float4(M, den, 0.f, 0.f);
+    if (lane == 0) *reinterpret_cast<float4*>(o) = make_float4(M, den, Mt, 0.f);
     *reinterpret_cast<float4*>(o + 4 + 4 * lane) = make_float4(nr[0], nr[1], nr[2], nr[3]);
     *reinterpret_cast<float4*>(o + 4 + D + 4 * lane) = make_float4(nw[0], nw[1], nw[2], nw[3]);
     return;
   }
   void* o = a.out_fp32 ? (void*)(static_cast<float*>(a.out) + (size_t)gw * D)
                        : (void*)(static_cast<uint16_t*>(a.out) + (size_t)gw * D);
-  finish(M, den, nr, nw, a.corr ? a.corr + (size_t)gw * (1 + D) : nullptr, a.literal, lane, o, a.out_fp32);
+  finish(M, Mt, den, nr, nw, a.corr ? a.corr + (size_t)gw * (1 + D) : nullptr, a.literal, lane, o,
+         a.out_fp32);
 }
 
 // LSE merge of n device records (m, l, y_rot, y_raw) + correction -> out.
@@ -810,8 +560,11 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
                                                             void* __restrict__ out) {
   const int gw = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (gw >= BH) return;
-  float M = -INFINITY;
-  for (int r = 0; r < n; ++r) M = fmaxf(M, recs[r * stride + (size_t)gw * PREC]);
+  float M = -INFINITY, Mt = -INFINITY;
+  for (int r = 0; r < n; ++r) {
+    M = fmaxf(M, recs[r * stride + (size_t)gw * PREC]);
+    Mt = fmaxf(Mt, recs[r * stride + (size_t)gw * PREC + 2]);
+  }
   float nr[4] = {0.f, 0.f, 0.f, 0.f}, nw[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
   if (M != -INFINITY) {
     for (int r = 0; r < n; ++r) {
@@ -829,12 +582,12 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
   }
   void* o = out_fp32 ? (void*)(static_cast<float*>(out) + (size_t)gw * D)
                      : (void*)(static_cast<uint16_t*>(out) + (size_t)gw * D);
-  finish(M, den, nr, nw, corr ? corr + (size_t)gw * (1 + D) : nullptr, literal, lane, o, out_fp32);
+  finish(M, Mt, den, nr, nw, corr ? corr + (size_t)gw * (1 + D) : nullptr, literal, lane, o, out_fp32);
 }
 
 // ------------------------------------------------------------- host ----
 struct Plan {
-  int NG, U, nsq, cpw, nrec, corr_on;
+  int NG, U, nsq, cpc, nrec, corr_on;
   size_t phi_off, corr_off, rec_off, total;
 };
 
@@ -846,15 +599,15 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   p.U = c->B * c->Hkv;
   int maxc = o && o->max_chunks_hint > 0 ? o->max_chunks_hint : c->max_chunks;
   int span = std::max(0, std::min(maxc, chunk_hi) - chunk_lo);
-  int cpw = o && o->chunks_per_split > 0 ? o->chunks_per_split : 0;
-  if (cpw == 0) {
-    // aim for ~16 warps of work per SM across the grid
-    long long warps_wanted = 148LL * 16;
-    long long chunks = (long long)p.U * std::max(span, 1);
-    cpw = (int)std::max(1LL, std::min(16LL, chunks / warps_wanted));
+  int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : 0;
+  if (cpc == 0) {
+    // ~2 waves of quantized-split CTAs at 4 resident CTAs per SM
+    const long long ctas_wanted = 148LL * 4 * 2;
+    const long long chunks = (long long)p.U * std::max(span, 1);
+    cpc = (int)std::max(2LL, std::min(32LL, (chunks + ctas_wanted - 1) / ctas_wanted));
   }
-  p.cpw = cpw;
-  p.nsq = std::max(1, (span + cpw * WARPS - 1) / (cpw * WARPS));
+  p.cpc = cpc;
+  p.nsq = std::max(1, (span + cpc - 1) / cpc);
   p.corr_on = corr_on && tail ? 1 : 0;
   p.nrec = p.nsq + (tail ? 2 : 0);
   size_t BH = (size_t)c->B * c->Hq;
@@ -868,12 +621,13 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
 template <int NG>
 int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, const Plan& p,
               char* ws, int chunk_lo, int chunk_hi, int tail, float* corr_ext, int literal,
-              int out_fp32, void* out, float* rec_out, cudaStream_t s) {
+              int out_fp32, void* out, float* rec_out, const kvlc_decode_opts* o, cudaStream_t s) {
   float* phi = reinterpret_cast<float*>(ws + p.phi_off);
   float* corr = corr_ext ? corr_ext : reinterpret_cast<float*>(ws + p.corr_off);
   float* rec = reinterpret_cast<float*>(ws + p.rec_off);
   if (p.corr_on) {
-    phi_kernel<NG><<<p.U, 256, 0, s>>>(*c, ad->w1q, ad->w2q, q, phi, corr);
+    phi_kernel<<<dim3(c->Hkv, (c->B * NG + PHI_QB - 1) / PHI_QB), 256, 0, s>>>(*c, NG, ad->w1q, ad->w2q, q,
+                                                                             phi, corr);
     int rc = check_launch("phi");
     if (rc) return rc;
   }
@@ -884,7 +638,7 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   a.corr = corr;
   a.rec = rec;
   a.nsq = p.nsq;
-  a.cpw = p.cpw;
+  a.cpc = p.cpc;
   a.chunk_lo = chunk_lo;
   a.chunk_hi = chunk_hi;
   a.tail = tail;
@@ -900,6 +654,10 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = p.corr_on ? 1 : 0;
+  if (o && o->ev_begin) {
+    KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_begin), s));
+    cfg.numAttrs = 0;  // the event already orders the launch
+  }
   if (NG <= 4) {
     KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a));
   } else {
@@ -915,6 +673,7 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
       default: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 3>, a)); break;
     }
   }
+  if (o && o->ev_end) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_end), s));
   CombArgs ca{};
   ca.B = c->B;
   ca.Hq = c->Hq;
@@ -940,11 +699,11 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
 
 int launch(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, const Plan& p, char* ws,
            int chunk_lo, int chunk_hi, int tail, float* corr_ext, int literal, int out_fp32, void* out,
-           float* rec_out, cudaStream_t s) {
+           float* rec_out, const kvlc_decode_opts* o, cudaStream_t s) {
   switch (p.NG) {
 #define KVLC_NG_CASE(n) \
   case n:               \
-    return launch_ng<n>(c, ad, q, p, ws, chunk_lo, chunk_hi, tail, corr_ext, literal, out_fp32, out, rec_out, s);
+    return launch_ng<n>(c, ad, q, p, ws, chunk_lo, chunk_hi, tail, corr_ext, literal, out_fp32, out, rec_out, o, s);
     KVLC_NG_CASE(1)
     KVLC_NG_CASE(2)
     KVLC_NG_CASE(3)
@@ -985,7 +744,7 @@ int kvlc_decode(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, 
   if (rc) return rc;
   KVLC_REQUIRE(ws && ws_bytes >= p.total, "decode workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
   return launch(c, ad, q, p, static_cast<char*>(ws), 0, 1 << 30, 1, nullptr, o ? o->literal : 0,
-                o ? o->out_fp32 : 0, out, nullptr, as_stream(stream));
+                o ? o->out_fp32 : 0, out, nullptr, o, as_stream(stream));
 }
 
 int kvlc_decode_partial(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q,
@@ -1003,7 +762,7 @@ int kvlc_decode_partial(const kvlc_cache* c, const kvlc_adapter* ad, const uint1
   if (include_tail && corr && !p.corr_on)
     KVLC_CUDA(cudaMemsetAsync(corr, 0, (size_t)c->B * c->Hq * (1 + D) * sizeof(float), as_stream(stream)));
   return launch(c, ad, q, p, static_cast<char*>(ws), chunk_lo, chunk_hi, include_tail ? 1 : 0, corr,
-                0, 0, nullptr, rec, as_stream(stream));
+                0, 0, nullptr, rec, o, as_stream(stream));
 }
 
 int kvlc_merge_records(const float* recs, int32_t n_rec, int64_t rec_stride, const float* corr,

@@ -50,8 +50,48 @@ __device__ __forceinline__ bool near_half_tie(double x) {
          __half_as_ushort(__double2half(x * (1.0 + 1e-12)));
 }
 
-__device__ __forceinline__ int vslot(int t) {  // device value-slot permutation (kvlinc.h)
-  return 16 * ((t & 31) >> 2) + 4 * (t >> 5) + (t & 3);
+// ---- fragment-native code layouts (include/kvlinc.h, consumed by kvlc_decode.cu) ----
+// Key word wi = ((w*32 + lane)*8 + kt), lane = 4g + t0: byte q holds channel
+// 16kt + 2t0 + {0,8,1,9}[q]; its bit pair j holds token 32w + 4g + j.
+__device__ __forceinline__ uint32_t pack_k_word(const uint8_t* codes, int wi) {
+  const int kt = wi & 7, lane = (wi >> 3) & 31, w = wi >> 8;
+  const int g = lane >> 2, t0 = lane & 3;
+  const int coff[4] = {0, 8, 1, 9};
+  uint32_t word = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      word |= (uint32_t)codes[(32 * w + 4 * g + j) * D + 16 * kt + 2 * t0 + coff[q]] << (8 * q + 2 * j);
+  return word;
+}
+
+// Value word wi = ((w*32 + lane)*8 + 4mt + p), lane = 4g + t0: byte q holds
+// token 32w + 8t0 + 2mt + {0,1,4,5}[q]; its bit pair j holds channel 32p + 8j + g.
+__device__ __forceinline__ uint32_t pack_v_word(const uint8_t* codes, int wi) {
+  const int i = wi & 7, lane = (wi >> 3) & 31, w = wi >> 8;
+  const int g = lane >> 2, t0 = lane & 3, mt = i >> 2, p = i & 3;
+  const int toff[4] = {0, 1, 4, 5};
+  uint32_t word = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      word |= (uint32_t)codes[(32 * w + 8 * t0 + 2 * mt + toff[q]) * D + 32 * p + 8 * j + g] << (8 * q + 2 * j);
+  return word;
+}
+
+// Code of (token t, channel c) of one chunk, from the device layouts above.
+__device__ __forceinline__ uint32_t k_code(const uint32_t* words, int t, int c) {
+  const int w = t >> 5, u = t & 31, g = u >> 2, j = u & 3;
+  const int kt = c >> 4, cc = c & 15, t0 = (cc & 7) >> 1, q = ((cc & 1) << 1) | (cc >> 3);
+  return (words[((w * 32) + 4 * g + t0) * 8 + kt] >> (8 * q + 2 * j)) & 3u;
+}
+
+__device__ __forceinline__ uint32_t v_code(const uint32_t* words, int t, int c) {
+  const int w = t >> 5, u = t & 31, t0 = u >> 3, hi = (u >> 2) & 1, mt = (u >> 1) & 1, lo = u & 1;
+  const int q = lo + 2 * hi, g = c & 7, r = (c >> 3) & 1, mv = c >> 4, p = mv >> 1, j = 2 * (mv & 1) + r;
+  return (words[((w * 32) + 4 * g + t0) * 8 + 4 * mt + p] >> (8 * q + 2 * j)) & 3u;
 }
 
 constexpr int MAX_B = 1024;
@@ -88,6 +128,7 @@ __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs
   float* kerr = smem;                       // [G][KERR_LD]
   float* vq = kerr + G * KERR_LD;           // [G][D]  (rotated basis)
   float* phi = vq + G * D;                  // [G][HALF]
+  uint8_t* codes_s = reinterpret_cast<uint8_t*>(phi);  // [G][D] codes, before phi is live
   const kvlc_cache& c = a.c;
   const int unit = blockIdx.y, split = blockIdx.x;
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
@@ -134,24 +175,23 @@ __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs
       double mx = (double)fmaxf(red_mx[ch], red_mx[ch + 128]);
       double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
       double inv = scale > 0.0 ? 1.0 / scale : 0.0;
-      for (int w = half * 4; w < half * 4 + 4; ++w) {
-        uint32_t word = 0;
 #pragma unroll 4
-        for (int i = 0; i < 16; ++i) {
-          int t = w * 16 + i;
-          double x = (double)bf2f(K[t * a.k_t + ch * a.k_c]);
-          uint32_t code = code2(x, mn, scale, inv);
-          word |= code << (2 * i);
-          double khat = __dadd_rn(__dmul_rn((double)code, scale), mn);
-          kerr[t * KERR_LD + ch] = (float)__dsub_rn(x, khat);
-        }
-        c.kcodes[(cb * 8 + w) * D + ch] = word;
+      for (int t = half * 64; t < half * 64 + 64; ++t) {
+        const double x = (double)bf2f(K[t * a.k_t + ch * a.k_c]);
+        const uint32_t code = code2(x, mn, scale, inv);
+        codes_s[t * D + ch] = (uint8_t)code;
+        const double khat = __dadd_rn(__dmul_rn((double)code, scale), mn);
+        kerr[t * KERR_LD + ch] = (float)__dsub_rn(x, khat);
       }
       if (half == 0) {
         c.kscale[cb * D + ch] = __half_as_ushort(__double2half(scale));
         c.kzero[cb * D + ch] = __half_as_ushort(__double2half(mn));
       }
     }
+    __syncthreads();
+    // pack the key codes into the decode kernel's fragment-native word layout
+    for (int wi = tid; wi < 1024; wi += FLUSH_THREADS) c.kcodes[cb * 1024 + wi] = pack_k_word(codes_s, wi);
+    __syncthreads();
 
     // ---- K2: values, FWHT post-rotation (fp64) then token-wise quantization ----
     for (int t = warp; t < G; t += FLUSH_THREADS / 32) {
@@ -215,27 +255,21 @@ __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs
         scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
         inv = scale > 0.0 ? 1.0 / scale : 0.0;
       }
-      uint32_t byte = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        uint32_t code = code2(x[e], mn, scale, inv);
-        byte |= code << (2 * e);
+        const uint32_t code = code2(x[e], mn, scale, inv);
+        codes_s[t * D + lane * 4 + e] = (uint8_t)code;
         vq[t * D + lane * 4 + e] = (float)__dadd_rn(__dmul_rn((double)code, scale), mn);
       }
-      uint32_t word = byte | (__shfl_down_sync(0xffffffffu, byte, 1) << 8) |
-                      (__shfl_down_sync(0xffffffffu, byte, 2) << 16) |
-                      (__shfl_down_sync(0xffffffffu, byte, 3) << 24);
-      if ((lane & 3) == 0) c.vcodes[(cb * 8 + (lane >> 2)) * G + vslot(t)] = word;
       if (lane == 0) {
         c.vscale[cb * G + t] = __half_as_ushort(__double2half(scale));
         c.vzero[cb * G + t] = __half_as_ushort(__double2half(mn));
       }
     }
-    if (!a.use_adapter) {
-      __syncthreads();
-      continue;
-    }
     __syncthreads();
+    for (int wi = tid; wi < 1024; wi += FLUSH_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word(codes_s, wi);
+    __syncthreads();
+    if (!a.use_adapter) continue;
 
     // ---- K3: phi_k(k_err) per token (two softmax halves), S += vq^T phi, P += sum phi ----
     const int tr = tid >> 4, fc = tid & 15;  // 16 x 16 thread tile, 8 x 8 outputs each
@@ -392,10 +426,19 @@ __global__ void append_finalize_kernel(kvlc_cache c, const SeqInfo seq) {
 __global__ void export_chunk_kernel(kvlc_cache c, int unit, int chunk, uint32_t* kw, uint32_t* vw,
                                     uint16_t* ks, uint16_t* kz, uint16_t* vs, uint16_t* vz) {
   const size_t cb = (size_t)unit * c.max_chunks + chunk;
+  const uint32_t* kwords = c.kcodes + cb * 1024;
+  const uint32_t* vwords = c.vcodes + cb * 1024;
   for (int i = threadIdx.x; i < 8 * 128; i += blockDim.x) {
-    kw[i] = c.kcodes[cb * 1024 + i];
-    int t = i / 8, j = i % 8;  // reference value_rows word (t, j)
-    vw[i] = c.vcodes[(cb * 8 + j) * G + vslot(t)];
+    // reference key word (w, ch): tokens 16w..16w+15 of channel ch (quantize.py:15-19)
+    const int w = i / 128, ch = i % 128;
+    uint32_t word = 0;
+    for (int l = 0; l < 16; ++l) word |= k_code(kwords, 16 * w + l, ch) << (2 * l);
+    kw[i] = word;
+    // reference value_rows word (t, j): channels 16j..16j+15 of token t
+    const int t = i / 8, j = i % 8;
+    word = 0;
+    for (int l = 0; l < 16; ++l) word |= v_code(vwords, t, 16 * j + l) << (2 * l);
+    vw[i] = word;
   }
   for (int i = threadIdx.x; i < 128; i += blockDim.x) {
     ks[i] = c.kscale[cb * D + i];

@@ -1,0 +1,468 @@
+// Quantized-split path of the fused decode (included by kvlc_decode.cu).
+//
+// A quantized-split CTA owns chunks [lo, hi) of one (b, kv-head) unit.  Its
+// 4 warps take the 4 32-token slices of every chunk:
+//   * each warp streams its slice (1 KB of K codes, 1 KB of V codes, the
+//     slice's V scale/zero and the K scale/zero of its B-operand share)
+//     through a 3-stage cp.async pipeline in shared memory;
+//   * the QK^T B operand of a chunk (q' = q * s_k, fp16 hi/lo) and the zero
+//     term zt = q . z_k are built cooperatively (warp w: k-tiles 2w, 2w+1),
+//     double-buffered in shared memory, one CTA barrier per chunk;
+//   * codes become fp16 MMA operands with one LOP3 per register (exact
+//     subnormals c * 4^j * 2^-24 from the fragment-native layouts written by
+//     kvlc_flush.cu); mma.sync m16n8k16, GQA heads on N;
+//   * online softmax in log2 units with lazy rescaling: the reference point
+//     only moves when the running max grows by more than LAZY (p <= 2^LAZY),
+//     the true max is tracked separately for literal-correction parity.
+#pragma once
+
+constexpr int STAGES = 3;
+constexpr float LAZY = 8.f;
+
+template <int NG>
+struct WarpState {
+  static constexpr bool HILO = NG <= 4;
+  static constexpr int NH = HILO ? 1 : 2;
+  float m[NH];      // reference point of p (log2 units)
+  float mt[NH];     // true running max
+  float l[NH], z[NH];
+  float acc[8][4];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int e = 0; e < NH; ++e) {
+      m[e] = -INFINITY;
+      mt[e] = -INFINITY;
+      l[e] = 0.f;
+      z[e] = 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  }
+};
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// One warp's data for one chunk.
+struct WarpStage {
+  uint4 k[2][32];   // K words 0-3 / 4-7 of each lane (fragment-native layout)
+  uint4 v[2][32];   // V words
+  uint2 vs[8];      // V scales of tokens 32w + 4g .. +3, per g
+  uint2 vz[8];
+  uint2 ks[8];      // K scales of channels 32w .. 32w+31 (the warp's B share)
+  uint2 kz[8];
+};
+
+struct QuantSmem {
+  WarpStage stage[STAGES][WARPS];
+  uint4 bq[2][4][32];   // [buf][k-tile pair][lane]: (b0, b1 of kt = 2p, b0, b1 of kt = 2p+1)
+  uint4 bl[2][4][32];   // low parts (groups of > 4 heads)
+  float4 zt[2][8];      // [buf][column g] -> partial zero terms of the 4 warps
+};
+
+union SplitSmem {
+  QuantSmem quant;
+  float rec[WARPS * 8 * REC];
+};
+
+// Per-lane source pointers of a warp's slice; every lane issues the same
+// cp.async sequence (2 x 16 B K, 2 x 16 B V, one 8 B metadata piece: lanes
+// 0-7 V scales, 8-15 V zeros, 16-23 K scales, 24-31 K zeros).  All sources
+// advance by a fixed stride per chunk.
+struct SliceSrc {
+  const uint4* k;     // advances 256 uint4 (4 KB) per chunk
+  const uint4* v;
+  const uint2* meta;  // advances 32 uint2 (256 B) per chunk
+  __device__ __forceinline__ void init(const kvlc_cache& c, size_t cb, int warp, int lane) {
+    k = reinterpret_cast<const uint4*>(c.kcodes + ((cb * 4 + warp) * 32 + lane) * 8);
+    v = reinterpret_cast<const uint4*>(c.vcodes + ((cb * 4 + warp) * 32 + lane) * 8);
+    const int role = lane >> 3, sub = lane & 7;
+    const uint16_t* base = role == 0 ? c.vscale : role == 1 ? c.vzero : role == 2 ? c.kscale : c.kzero;
+    meta = reinterpret_cast<const uint2*>(base + cb * 128 + 32 * warp + 4 * sub);
+  }
+  __device__ __forceinline__ void issue(WarpStage& st, int lane, int chunk_off) const {
+    const uint4* kp = k + (size_t)chunk_off * 256;
+    const uint4* vp = v + (size_t)chunk_off * 256;
+    cp_async16(&st.k[0][lane], kp);
+    cp_async16(&st.k[1][lane], kp + 1);
+    cp_async16(&st.v[0][lane], vp);
+    cp_async16(&st.v[1][lane], vp + 1);
+    cp_async8(&st.vs[0] + lane, meta + (size_t)chunk_off * 32);   // vs, vz, ks, kz are contiguous
+  }
+};
+
+// Builds this warp's share (k-tiles 2w, 2w+1) of a chunk's B operand from its stage.
+//  HILO: column n = g holds head g>>1: the hi part for even g, the lo part
+//        (exact FMA residual q*s - hi) for odd g.
+//  else: column n = g holds head g (hi in bq, lo in bl).
+template <int NG>
+__device__ __forceinline__ void build_b(QuantSmem& sm, int buf, const WarpStage& st,
+                                        const uint32_t (&qs)[4], int warp, int lane) {
+  constexpr bool HILO = NG <= 4;
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t* ks = reinterpret_cast<const uint32_t*>(st.ks);
+  const uint32_t* kz = reinterpret_cast<const uint32_t*>(st.kz);
+  uint32_t b[4], bl[4];
+  float zp = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    // i = 2e + k: channels 32w + 16e + 2t + {0,1} (+8 for k = 1)
+    const int pair = 8 * (i >> 1) + t + 4 * (i & 1);
+    const __half2 qv = u2h(qs[i]), sv = u2h(ks[pair]);
+    const __half2 hi = __hmul2(qv, sv);
+    if (HILO) {
+      const uint32_t neg = (g & 1) ? (h2u(hi) ^ 0x80008000u) : 0u;
+      b[i] = h2u(__hfma2(qv, sv, u2h(neg)));
+    } else {
+      b[i] = h2u(hi);
+      bl[i] = h2u(__hfma2(qv, sv, __hneg2(hi)));
+    }
+    const float2 qf = __half22float2(qv), zf = __half22float2(u2h(kz[pair]));
+    zp = fmaf(qf.x, zf.x, zp);
+    zp = fmaf(qf.y, zf.y, zp);
+  }
+  sm.bq[buf][warp][lane] = make_uint4(b[0], b[1], b[2], b[3]);
+  if (!HILO) sm.bl[buf][warp][lane] = make_uint4(bl[0], bl[1], bl[2], bl[3]);
+  zp += __shfl_xor_sync(0xffffffffu, zp, 1);
+  zp += __shfl_xor_sync(0xffffffffu, zp, 2);
+  if (t == 0) reinterpret_cast<float*>(&sm.zt[buf][g])[warp] = zp;
+}
+
+// One 128-token chunk, this warp's 32-token slice (tokens 32w .. 32w+31).
+// K word kt of lane (g, t) holds channels 16kt+2t+{0,8,1,9} in bytes 0..3 and
+// tokens 32w+4g+j at bits 2j; V word 4mt+p holds tokens 32w+8t+2mt+{0,1,4,5}
+// in bytes 0..3 and channels 32p+8j+g at bits 2j.
+template <int NG, int EXTRA>
+__device__ __forceinline__ void quant_chunk(const WarpStage& stg, const QuantSmem& sm, int buf,
+                                            WarpState<NG>& st, int lane) {
+  constexpr bool HILO = NG <= 4;
+  constexpr int NH = WarpState<NG>::NH;
+  constexpr bool QK_LO = !HILO && (EXTRA & 1);
+  constexpr bool PV_LO = !HILO && (EXTRA & 2);
+  const int g = lane >> 2, t = lane & 3;
+
+  float zt[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) {
+    const float4 zz = sm.zt[buf][HILO ? 2 * t : 2 * t + e];
+    zt[e] = ((zz.x + zz.y) + (zz.z + zz.w)) * C0;
+  }
+
+  // ---- Q K^T over the slice's 2 token tiles ----
+  float cq[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cq[i][j] = 0.f;
+  {
+    const uint4 k0 = stg.k[0][lane], k1 = stg.k[1][lane];
+    const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint4 b = sm.bq[buf][p][lane];
+      uint4 bl = make_uint4(0u, 0u, 0u, 0u);
+      if (QK_LO) bl = sm.bl[buf][p][lane];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t x = kw[2 * p + e], y = x >> 8;
+        const uint32_t b0 = e ? b.z : b.x, b1 = e ? b.w : b.y;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const uint32_t a0 = code_h2(x, 2 * mt), a1 = code_h2(x, 2 * mt + 1);
+          const uint32_t a2 = code_h2(y, 2 * mt), a3 = code_h2(y, 2 * mt + 1);
+          mma_f16(cq[mt], a0, a1, a2, a3, b0, b1);
+          if (QK_LO) mma_f16(cq[mt], a0, a1, a2, a3, e ? bl.z : bl.x, e ? bl.w : bl.y);
+        }
+      }
+    }
+  }
+
+  // ---- online softmax: thread holds tokens 32w + 4g + (2mt + r) ----
+  float cmax[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) cmax[e] = -INFINITY;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float F = code_unscale(2 * mt + r) * C0;
+      if (HILO) {
+        const float v = fmaf(cq[mt][2 * r] + cq[mt][2 * r + 1], F, zt[0]);
+        cq[mt][2 * r] = v;
+        cmax[0] = fmaxf(cmax[0], v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float v = fmaf(cq[mt][2 * r + e], F, zt[e]);
+          cq[mt][2 * r + e] = v;
+          cmax[e] = fmaxf(cmax[e], v);
+        }
+      }
+    }
+  }
+  bool grow = false;
+  float mref[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) {
+    float m = cmax[e];
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+    st.mt[e] = fmaxf(st.mt[e], m);
+    // move the reference point only when p would exceed 2^LAZY
+    mref[e] = m > st.m[e] + LAZY ? m : st.m[e];
+    grow |= mref[e] != st.m[e];
+  }
+  if (__any_sync(0xffffffffu, grow)) {
+    float sc[NH];
+#pragma unroll
+    for (int e = 0; e < NH; ++e) {
+      sc[e] = fast_exp2(st.m[e] - mref[e]);   // exp2(-inf) = 0 on the first chunk
+      st.m[e] = mref[e];
+      st.l[e] *= sc[e];
+      st.z[e] *= sc[e];
+    }
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+      if (HILO) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) st.acc[mv][j] *= sc[0];
+      } else {
+        st.acc[mv][0] *= sc[0];
+        st.acc[mv][2] *= sc[0];
+        st.acc[mv][1] *= sc[1];
+        st.acc[mv][3] *= sc[1];
+      }
+    }
+  }
+  const uint2 vs = stg.vs[g], vz = stg.vz[g];
+  const float2 s01 = __half22float2(u2h(vs.x)), s23 = __half22float2(u2h(vs.y));
+  const float2 z01 = __half22float2(u2h(vz.x)), z23 = __half22float2(u2h(vz.y));
+  const float svs[4] = {s01.x, s01.y, s23.x, s23.y}, svz[4] = {z01.x, z01.y, z23.x, z23.y};
+  uint32_t bp[2][2], bpl[2][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float sv = svs[2 * mt + r], zv = svz[2 * mt + r];
+      if (HILO) {
+        const float p = fast_exp2(cq[mt][2 * r] - st.m[0]);
+        st.l[0] += p;
+        st.z[0] = fmaf(p, zv, st.z[0]);
+        const float pv = p * sv;
+        // hi: pv truncated to 11 significant bits (fp16-exact), lo: the exact remainder
+        const float hi = __uint_as_float(__float_as_uint(pv) & 0xffffe000u);
+        bp[mt][r] = movm_t(h2u(__floats2half2_rn(hi, pv - hi)));
+      } else {
+        const float p0 = fast_exp2(cq[mt][2 * r] - st.m[0]);
+        const float p1 = fast_exp2(cq[mt][2 * r + 1] - st.m[1]);
+        st.l[0] += p0;
+        st.l[1] += p1;
+        st.z[0] = fmaf(p0, zv, st.z[0]);
+        st.z[1] = fmaf(p1, zv, st.z[1]);
+        const float a0 = p0 * sv, a1 = p1 * sv;
+        const __half2 hh = __floats2half2_rn(a0, a1);
+        bp[mt][r] = movm_t(h2u(hh));
+        if (PV_LO) {
+          const float2 hf = __half22float2(hh);
+          bpl[mt][r] = movm_t(h2u(__floats2half2_rn(a0 - hf.x, a1 - hf.y)));
+        }
+      }
+    }
+  }
+
+  // ---- P V: 8 channel tiles x the slice's 2 token tiles ----
+  const uint4 v0 = stg.v[0][lane], v1 = stg.v[1][lane];
+  const uint32_t vw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t x = vw[4 * mt + p], y = x >> 8;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int mv = 2 * p + h;
+        const uint32_t a0 = code_h2(x, 2 * h), a1 = code_h2(x, 2 * h + 1);
+        const uint32_t a2 = code_h2(y, 2 * h), a3 = code_h2(y, 2 * h + 1);
+        mma_f16(st.acc[mv], a0, a1, a2, a3, bp[mt][0], bp[mt][1]);
+        if (PV_LO) mma_f16(st.acc[mv], a0, a1, a2, a3, bpl[mt][0], bpl[mt][1]);
+      }
+    }
+  }
+}
+
+// Writes this warp's record (m_ref, l, m_true, -, y[c]) per head into shared memory.
+// Quantized rows: channel 16mv + g + 8r with factor 2^24 4^-(2(mv&1)+r), plus
+// the value zero term; residual rows: channel 16mv + g + 8r, no factor.
+template <int NG, bool QUANT>
+__device__ __forceinline__ void warp_store(WarpState<NG>& st, float* smrec, int lane) {
+  constexpr bool HILO = NG <= 4;
+  constexpr int NH = WarpState<NG>::NH;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int e = 0; e < NH; ++e) {
+    float l = st.l[e], z = st.z[e];
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      l += __shfl_xor_sync(0xffffffffu, l, o);
+      z += __shfl_xor_sync(0xffffffffu, z, o);
+    }
+    st.l[e] = l;
+    st.z[e] = z;
+  }
+#pragma unroll
+  for (int e = 0; e < NH; ++e) {
+    const int h = HILO ? t : 2 * t + e;
+    if (h >= NG) continue;
+    float* r = smrec + h * REC;
+    if (g == 0) {
+      r[0] = st.m[e];
+      r[1] = st.l[e];
+      r[2] = st.mt[e];
+    }
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        float v = HILO ? st.acc[mv][2 * rr] + st.acc[mv][2 * rr + 1] : st.acc[mv][2 * rr + e];
+        if (QUANT) v = fmaf(v, code_unscale(2 * (mv & 1) + rr), st.z[e]);
+        r[4 + 16 * mv + g + 8 * rr] = v;
+      }
+    }
+  }
+}
+
+// Merges the WARPS per-warp records in shared memory into one global record per head.
+// (the caller has synchronised after warp_store)
+template <int NG>
+__device__ __forceinline__ void cta_merge(float* sm, float* out) {
+  __shared__ float wts[NG][WARPS];
+  __shared__ float hdr[NG][4];
+  if (threadIdx.x < NG) {
+    const int h = threadIdx.x;
+    float M = -INFINITY, Mt = -INFINITY, l = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      M = fmaxf(M, sm[(w * NG + h) * REC]);
+      Mt = fmaxf(Mt, sm[(w * NG + h) * REC + 2]);
+    }
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      const float mw = sm[(w * NG + h) * REC];
+      const float wt = mw == -INFINITY ? 0.f : exp2f(mw - M);
+      wts[h][w] = wt;
+      l = fmaf(wt, sm[(w * NG + h) * REC + 1], l);
+    }
+    hdr[h][0] = M;
+    hdr[h][1] = l;
+    hdr[h][2] = Mt;
+    hdr[h][3] = 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NG * (D / 4 + 1); i += THREADS) {
+    const int h = i / (D / 4 + 1), k4 = i % (D / 4 + 1);
+    float4 v;
+    if (k4 == 0) {
+      v = make_float4(hdr[h][0], hdr[h][1], hdr[h][2], 0.f);
+    } else {
+      v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) {
+        const float wt = wts[h][w];
+        const float4 y = reinterpret_cast<const float4*>(sm + (w * NG + h) * REC)[k4];
+        v.x = fmaf(wt, y.x, v.x);
+        v.y = fmaf(wt, y.y, v.y);
+        v.z = fmaf(wt, y.z, v.z);
+        v.w = fmaf(wt, y.w, v.w);
+      }
+    }
+    reinterpret_cast<float4*>(out + h * REC)[k4] = v;
+  }
+}
+
+// A quantized split: chunks [lo, hi) of one unit.
+template <int NG, int EXTRA>
+__device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) {
+  const kvlc_cache& c = a.c;
+  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr bool HILO = NG <= 4;
+  // q (fp16, exact from bf16) for this warp's B share: column n = g,
+  // channels 32w + 16e + 2t + {0,1} (+8)
+  uint32_t qs[4];
+  {
+    const int head = HILO ? (g >> 1) : g;
+    const bool valid = head < NG;
+    const uint32_t* qp = reinterpret_cast<const uint32_t*>(
+        a.q + ((size_t)b * c.Hq + (size_t)kvh * NG + (valid ? head : 0)) * D);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int pair = 16 * warp + 8 * (i >> 1) + t + 4 * (i & 1);
+      const uint32_t raw = valid ? __ldg(qp + pair) : 0u;
+      qs[i] = h2u(__floats2half2_rn(__uint_as_float(raw << 16), __uint_as_float(raw & 0xffff0000u)));
+    }
+  }
+  WarpState<NG> st;
+  st.init();
+  const int n_ch = min(c.n_chunks[b], a.chunk_hi);
+  const int lo = a.chunk_lo + split * a.cpc;
+  const int hi = min(n_ch, lo + a.cpc);
+  const size_t cb0 = (size_t)unit * c.max_chunks;
+  QuantSmem& q = sm.quant;
+  if (lo < hi) {
+    SliceSrc src;
+    src.init(c, cb0 + lo, warp, lane);
+    const int n = hi - lo;
+    // prologue: stages for chunks 0, 1 (relative) in flight
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < n) src.issue(q.stage[s][warp], lane, s);
+      cp_commit();
+    }
+    cp_wait<STAGES - 2>();
+    __syncwarp();
+    build_b<NG>(q, 0, q.stage[0][warp], qs, warp, lane);
+    __syncthreads();
+    int s_cur = 0;
+    for (int k = 0; k < n; ++k) {
+      const int buf = k & 1;
+      const int s_next = s_cur == STAGES - 1 ? 0 : s_cur + 1;
+      const int s_fill = s_cur == 0 ? STAGES - 1 : s_cur - 1;   // freed by chunk k-1
+      if (k + STAGES - 1 < n) src.issue(q.stage[s_fill][warp], lane, k + STAGES - 1);
+      cp_commit();
+      quant_chunk<NG, EXTRA>(q.stage[s_cur][warp], q, buf, st, lane);
+      if (k + 1 < n) {
+        cp_wait<STAGES - 2>();   // chunk k+1 has landed (only k+2 may be pending)
+        __syncwarp();
+        build_b<NG>(q, buf ^ 1, q.stage[s_next][warp], qs, warp, lane);
+      }
+      __syncthreads();
+      s_cur = s_next;
+    }
+    cp_wait<0>();
+  }
+  __syncthreads();   // the record area aliases the pipeline buffers
+  warp_store<NG, true>(st, sm.rec + warp * NG * REC, lane);
+  __syncthreads();
+  cta_merge<NG>(sm.rec, a.rec + ((size_t)unit * a.nrec + split) * NG * REC);
+}
