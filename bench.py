@@ -223,8 +223,9 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": B * world / (e2e_ms * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": B * HQ * D * 2, "d2h_bytes_per_step": B * HQ * D * 2,
                 "ms_per_step": e2e_ms},
-        "gpu_launches": 3 * K,
-        "launch": "CUDA graph per step (phi_kernel -> split_kernel -> combine_kernel, PDL-chained)",
+        "gpu_launches": 2 * K,
+        "launch": "CUDA graph per step: phi_kernel -> split_kernel (PDL-chained; LSE combine fused "
+                  "into the last CTA of each unit)",
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_fa:

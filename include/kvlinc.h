@@ -214,7 +214,10 @@ typedef struct kvlc_decode_opts {
 
 /* Fused GQA decode (Algorithm 1 / decode_step_blocked, attention.py:197-276)
  * for every (b, q-head): q bf16 [B][Hq][128] -> out bf16 [B][Hq][128].
- * Launches phi_q, the split-KV kernel and the LSE combine. */
+ * Launches phi_q and the split-KV kernel (PDL-chained); the last CTA of each
+ * (b, kv-head) unit performs the LSE combine.  The workspace must be
+ * zero-filled before its first use (its head holds per-unit arrival counters
+ * that every launch leaves at zero). */
 size_t kvlc_decode_workspace(const kvlc_cache* cache, const kvlc_decode_opts* o);
 int kvlc_decode(const kvlc_cache* cache, const kvlc_adapter* ad,
                 const uint16_t* q, void* out, const kvlc_decode_opts* o,

@@ -127,9 +127,17 @@ class BatchedKVCache:
                          p(self.res_start_dev), p(self.res_len_dev))
 
     def workspace(self, nbytes: int) -> torch.Tensor:
+        """Scratch for prefill / append (contents are transient)."""
         if self._ws is None or self._ws.numel() < nbytes:
             self._ws = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
         return self._ws
+
+    def decode_ws(self, nbytes: int) -> torch.Tensor:
+        """Decode workspace: zero-filled once; its head holds the per-unit arrival
+        counters of the fused combine, which every decode launch leaves at zero."""
+        if getattr(self, "_dws", None) is None or self._dws.numel() < nbytes:
+            self._dws = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=self.device)
+        return self._dws
 
     @property
     def tokens(self) -> np.ndarray:
@@ -217,7 +225,7 @@ class BatchedKVCache:
             raise ValueError("out must be a [B, Hq, 128] bf16 or float32 tensor")
         o = self._opts(literal, chunks_per_split, out.dtype == torch.float32, events)
         nbytes = _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
-        ws = self.workspace(nbytes)
+        ws = self.decode_ws(nbytes)
         ad = _adapter_struct(adapters)
         _lib.call("kvlc_decode", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(q), _ptr(out),
                   ctypes.byref(o), _ptr(ws), ws.numel(), _lib.stream_handle())
@@ -226,7 +234,7 @@ class BatchedKVCache:
     def capture_decode(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False,
                        out: torch.Tensor | None = None, chunks_per_split: int = 0):
         """Capture one decode step on fixed q / out buffers into a CUDA graph
-        (the three PDL-chained launches replay with one graph launch).
+        (the PDL-chained launches replay with one graph launch).
         Returns (graph, out); refill q in place and call graph.replay()."""
         if out is None:
             out = torch.empty(q.shape, dtype=torch.bfloat16, device=self.device)
@@ -251,7 +259,7 @@ class BatchedKVCache:
             corr = torch.zeros((self.B, self.Hq, CORR_FLOATS), dtype=torch.float32, device=self.device)
         o = self._opts(False, chunks_per_split)
         nbytes = _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
-        ws = self.workspace(nbytes)
+        ws = self.decode_ws(nbytes)
         ad = _adapter_struct(adapters)
         _lib.call("kvlc_decode_partial", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(q),
                   int(chunk_lo), int(chunk_hi), int(bool(include_tail)), _ptr(rec),

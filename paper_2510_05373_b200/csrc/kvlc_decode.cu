@@ -7,18 +7,20 @@
 // e^{-M}-consistent rule (_reduce_blocks, attention.py:158-194), the inverse
 // Hadamard rotation of the quantized numerator and the final divide.
 //
-// Kernels (one decode step = 3 launches, PDL-chained):
+// Kernels (one decode step = 2 launches, PDL-chained):
 //   phi_kernel      phi_q(q) per q-head and C_d = P . phi      (attention.py:224-228)
-//   split_kernel    per CTA task, warp-specialised by blockIdx:
+//   split_kernel    per CTA task, selected by blockIdx:
 //                   * quantized split: chunks of one (b, kv-head) unit, GQA
 //                     heads batched on the MMA N dimension, 2-bit codes turned
 //                     into fp16 MMA operands by one LOP3 each (exact subnormal
 //                     values c * 4^j * 2^-24), scales folded into q / p
 //                     (hi+lo fp16 split when the group has <= 4 heads)
+//                     (kvlc_quant.cuh)
 //                   * residual half: bf16 ring window, masked
 //                   * correction rows: C_n = S phi for 32 rows of S
-//   combine_kernel  LSE merge of the split records + correction, warp FWHT
-//                   (H^T = H), divide, bf16 out.
+//                   the last CTA of each unit performs the LSE merge of the
+//                   unit's records + correction, the warp FWHT (H^T = H) and
+//                   the divide (no separate combine launch).
 //
 // Online-softmax state is kept in log2 units (logit * log2 e); the sign of the
 // global max, which selects the correction branch, is unit independent.
@@ -111,6 +113,12 @@ struct DecArgs {
   int tail;               // include residual window + correction rows
   int corr_on;            // adapter active
   int nrec;               // records per unit = nsq + 2*tail
+  // fused LSE combine: the last CTA of a unit merges its records
+  uint32_t* done;         // [U] arrival counters (zeroed before the launch, self-cleaning)
+  int literal;
+  int out_fp32;
+  void* out;              // [B][Hq][D] bf16 / f32 (final output)
+  float* rec_out;         // partial mode: [B][Hq][PREC] (split-KV across devices)
 };
 
 // ---------------------------------------------------------------- phi_q ----
@@ -384,27 +392,6 @@ __device__ void run_corr(const DecArgs& a, int unit, int rb) {
   }
 }
 
-template <int NG, int EXTRA>
-__global__ void __launch_bounds__(THREADS, 4) split_kernel(const DecArgs a) {
-  __shared__ __align__(16) SplitSmem sm;
-  float* smrec = sm.rec;
-  const int U = a.c.B * a.c.Hkv;
-  int x = blockIdx.x;
-  if (x < U * a.nsq) {
-    run_quant<NG, EXTRA>(a, x / a.nsq, x % a.nsq, sm);
-    return;
-  }
-  x -= U * a.nsq;
-  if (a.tail) {
-    if (x < 2 * U) {
-      run_resid<NG>(a, x / 2, x % 2, smrec);
-      return;
-    }
-    x -= 2 * U;
-    if (a.corr_on && x < U * CORR_CTAS) run_corr<NG>(a, x / CORR_CTAS, x % CORR_CTAS);
-  }
-}
-
 // ------------------------------------------------------------ combine ----
 // FWHT of 128 values, 4 per lane (channels 4 lane + e), unnormalised.
 __device__ __forceinline__ void warp_fwht128(float (&x)[4], int lane) {
@@ -423,18 +410,6 @@ __device__ __forceinline__ void warp_fwht128(float (&x)[4], int lane) {
   }
 }
 
-struct CombArgs {
-  int B, Hq, NG, Hkv;
-  const float* rec;  // decode: [U][nrec][NG][REC];  merge: [n][B][Hq][2+2D] with stride
-  int nrec, nsq;     // decode mode
-  int64_t rec_stride;
-  const float* corr;  // [B][Hq][1+D] or null
-  int literal;
-  int out_fp32;
-  void* out;          // [B][Hq][D] bf16 or f32 (final)
-  float* rec_out;     // partial mode: [B][Hq][2+2D]
-};
-
 // Shared tail: apply the correction rule and produce out = (H num_rot + num_raw)/den.
 // num/den are expressed in the frame 2^-M (M = max of the records' reference
 // points); Mt is the true global logit max (the reference's M, attention.py:172-175).
@@ -442,6 +417,7 @@ struct CombArgs {
 // M >= 0, else the blocks are scaled by 2^M (attention.py:190-194); both are the
 // same value as the reference's e^-M_true form.  Literal mode adds C unscaled in
 // the true-max frame (attention.py:188-189).
+// corr: nullptr, or {C_d, C_n[4*lane .. 4*lane+3]} of this lane.
 __device__ __forceinline__ void finish(float M, float Mt, float den, float (&nr)[4], float (&nw)[4],
                                        const float* corr, int literal, int lane, void* out,
                                        int out_fp32) {
@@ -449,7 +425,7 @@ __device__ __forceinline__ void finish(float M, float Mt, float den, float (&nr)
     const float cd = corr[0];
     float cn[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) cn[e] = corr[1 + 4 * lane + e];
+    for (int e = 0; e < 4; ++e) cn[e] = corr[1 + e];
     bool any = cd != 0.f || cn[0] != 0.f || cn[1] != 0.f || cn[2] != 0.f || cn[3] != 0.f;
     any = __any_sync(0xffffffffu, any);
     if (any) {
@@ -491,22 +467,21 @@ __device__ __forceinline__ void finish(float M, float Mt, float den, float (&nr)
   }
 }
 
-__global__ void __launch_bounds__(128) combine_kernel(const CombArgs a) {
-  griddep_wait();
-  const int gw = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (gw >= a.B * a.Hq) return;
-  const int b = gw / a.Hq, qh = gw % a.Hq, kvh = qh / a.NG, h = qh % a.NG;
-  const int unit = b * a.Hkv + kvh;
-  const float* base = a.rec + (size_t)unit * a.nrec * a.NG * REC + (size_t)h * REC;
-  const size_t rstride = (size_t)a.NG * REC;
-  // lanes hold the records' (m, l); weights via one warp max / sum, then the
-  // numerators stream with independent loads.
+// LSE merge of one (b, q-head)'s split records (+ the correction) by one warp:
+// lanes hold the records' (m, l) for the weights, the numerators stream with
+// independent loads; records are read with ld.global.cg (written by other CTAs
+// of the same launch).
+__device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, int h_local, int kvh,
+                                             int lane) {
+  const int unit = b * a.c.Hkv + kvh, qh = kvh * NG + h_local, gw = b * a.c.Hq + qh;
+  const float* base = a.rec + (size_t)unit * a.nrec * NG * REC + (size_t)h_local * REC;
+  const size_t rstride = (size_t)NG * REC;
   float M = -INFINITY, Mt = -INFINITY;
   for (int r0 = 0; r0 < a.nrec; r0 += 32) {
     const int r = r0 + lane;
     if (r < a.nrec) {
-      M = fmaxf(M, base[r * rstride]);
-      Mt = fmaxf(Mt, base[r * rstride + 2]);
+      M = fmaxf(M, __ldcg(base + r * rstride));
+      Mt = fmaxf(Mt, __ldcg(base + r * rstride + 2));
     }
   }
   M = warp_max(M);
@@ -517,14 +492,14 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombArgs a) {
       const int r = r0 + lane, cnt = min(32, a.nrec - r0);
       float w = 0.f;
       if (r < a.nrec) {
-        const float m = base[r * rstride];
+        const float m = __ldcg(base + r * rstride);
         w = m == -INFINITY ? 0.f : exp2f(m - M);
-        den = fmaf(w, base[r * rstride + 1], den);
+        den = fmaf(w, __ldcg(base + r * rstride + 1), den);
       }
 #pragma unroll 4
       for (int i = 0; i < cnt; ++i) {
         const float wi = __shfl_sync(0xffffffffu, w, i);
-        const float4 y = *reinterpret_cast<const float4*>(base + (r0 + i) * rstride + 4 + 4 * lane);
+        const float4 y = __ldcg(reinterpret_cast<const float4*>(base + (r0 + i) * rstride + 4) + lane);
         if (r0 + i < a.nsq) {  // warp-uniform: quantized (rotated) vs residual (raw) basis
           nr[0] = fmaf(wi, y.x, nr[0]);
           nr[1] = fmaf(wi, y.y, nr[1]);
@@ -540,7 +515,7 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombArgs a) {
     }
     den = warp_sum(den);
   }
-  if (a.rec_out) {  // partial mode: (M, den, num_rot, num_raw), no correction
+  if (a.rec_out) {  // partial mode: (M, den, Mt, 0, num_rot, num_raw), no correction
     float* o = a.rec_out + (size_t)gw * PREC;
     if (lane == 0) *reinterpret_cast<float4*>(o) = make_float4(M, den, Mt, 0.f);
     *reinterpret_cast<float4*>(o + 4 + 4 * lane) = make_float4(nr[0], nr[1], nr[2], nr[3]);
@@ -549,8 +524,54 @@ __global__ void __launch_bounds__(128) combine_kernel(const CombArgs a) {
   }
   void* o = a.out_fp32 ? (void*)(static_cast<float*>(a.out) + (size_t)gw * D)
                        : (void*)(static_cast<uint16_t*>(a.out) + (size_t)gw * D);
-  finish(M, Mt, den, nr, nw, a.corr ? a.corr + (size_t)gw * (1 + D) : nullptr, a.literal, lane, o,
-         a.out_fp32);
+  const float* corr = a.corr_on ? a.corr + (size_t)gw * (1 + D) : nullptr;
+  float cbuf[1 + 4];
+  if (corr) {  // correction rows were written by other CTAs: read through L2
+    cbuf[0] = __ldcg(corr);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cbuf[1 + e] = __ldcg(corr + 1 + 4 * lane + e);  // rows are 129 floats
+  }
+  finish(M, Mt, den, nr, nw, corr ? cbuf : nullptr, a.literal, lane, o, a.out_fp32);
+}
+
+// The whole decode step's split-KV work in one launch; blockIdx selects the
+// task: quantized splits, residual halves, correction rows.  Every CTA bumps
+// its unit's arrival counter after publishing its record; the last one
+// performs the LSE combine of the unit (no separate combine launch).
+template <int NG, int EXTRA>
+__global__ void __launch_bounds__(THREADS, 4) split_kernel(const DecArgs a) {
+  __shared__ __align__(16) SplitSmem sm;
+  __shared__ int last;
+  const int U = a.c.B * a.c.Hkv;
+  int x = blockIdx.x, unit;
+  if (x < U * a.nsq) {
+    unit = x / a.nsq;
+    run_quant<NG, EXTRA>(a, unit, x % a.nsq, sm);
+  } else {
+    x -= U * a.nsq;
+    if (x < 2 * U) {
+      unit = x / 2;
+      run_resid<NG>(a, unit, x % 2, sm.rec);
+    } else {
+      x -= 2 * U;
+      unit = x / CORR_CTAS;
+      run_corr<NG>(a, unit, x % CORR_CTAS);
+    }
+  }
+  const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? CORR_CTAS : 0) : 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();  // publish this CTA's record / correction rows
+    last = atomicAdd(a.done + unit, 1u) == (uint32_t)(per_unit - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (a.corr_on) griddep_wait();  // C_d comes from phi_kernel
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = unit / a.c.Hkv, kvh = unit % a.c.Hkv;
+  for (int h = warp; h < NG; h += WARPS) combine_head(a, NG, b, h, kvh, lane);
+  if (threadIdx.x == 0) a.done[unit] = 0u;  // self-cleaning for the next step
 }
 
 // LSE merge of n device records (m, l, y_rot, y_raw) + correction -> out.
@@ -582,13 +603,20 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
   }
   void* o = out_fp32 ? (void*)(static_cast<float*>(out) + (size_t)gw * D)
                      : (void*)(static_cast<uint16_t*>(out) + (size_t)gw * D);
-  finish(M, Mt, den, nr, nw, corr ? corr + (size_t)gw * (1 + D) : nullptr, literal, lane, o, out_fp32);
+  float cbuf[5];
+  if (corr) {
+    const float* cp = corr + (size_t)gw * (1 + D);
+    cbuf[0] = cp[0];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cbuf[1 + e] = cp[1 + 4 * lane + e];
+  }
+  finish(M, Mt, den, nr, nw, corr ? cbuf : nullptr, literal, lane, o, out_fp32);
 }
 
 // ------------------------------------------------------------- host ----
 struct Plan {
   int NG, U, nsq, cpc, nrec, corr_on;
-  size_t phi_off, corr_off, rec_off, total;
+  size_t done_off, phi_off, corr_off, rec_off, total;
 };
 
 int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int chunk_hi, int tail,
@@ -614,6 +642,13 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   p.phi_off = 0;
   p.corr_off = align_up(BH * RANK * sizeof(float));
   p.rec_off = p.corr_off + align_up(BH * (1 + D) * sizeof(float));
+  // arrival counters first: their offset must not depend on the split plan
+  // (they are zero-initialised once and left at zero by every launch)
+  p.done_off = 0;
+  const size_t base = align_up((size_t)p.U * sizeof(uint32_t));
+  p.phi_off += base;
+  p.corr_off += base;
+  p.rec_off += base;
   p.total = p.rec_off + align_up((size_t)p.U * p.nrec * p.NG * REC * sizeof(float));
   return KVLC_OK;
 }
@@ -644,6 +679,11 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   a.tail = tail;
   a.corr_on = p.corr_on;
   a.nrec = p.nrec;
+  a.done = reinterpret_cast<uint32_t*>(ws + p.done_off);
+  a.literal = literal;
+  a.out_fp32 = out_fp32;
+  a.out = out;
+  a.rec_out = rec_out;
   int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? p.U * CORR_CTAS : 0) : 0);
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
@@ -674,26 +714,6 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     }
   }
   if (o && o->ev_end) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_end), s));
-  CombArgs ca{};
-  ca.B = c->B;
-  ca.Hq = c->Hq;
-  ca.NG = NG;
-  ca.Hkv = c->Hkv;
-  ca.rec = rec;
-  ca.nrec = p.nrec;
-  ca.nsq = p.nsq;
-  ca.corr = p.corr_on ? corr : nullptr;
-  ca.literal = literal;
-  ca.out_fp32 = out_fp32;
-  ca.out = out;
-  ca.rec_out = rec_out;
-  cudaLaunchConfig_t cfg2{};
-  cfg2.gridDim = dim3((c->B * c->Hq + 3) / 4);
-  cfg2.blockDim = dim3(128);
-  cfg2.stream = s;
-  cfg2.attrs = attr;
-  cfg2.numAttrs = 1;
-  KVLC_CUDA(cudaLaunchKernelEx(&cfg2, combine_kernel, ca));
   return check_launch("decode");
 }
 
