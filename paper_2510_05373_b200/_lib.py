@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, c_float, c_int, c_int32, c_int64, c_size_t, c_uint16, c_uint32, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkvlinc.so")
+LIB_PATH = os.environ.get("KVLC_LIB") or os.path.join(_HERE, "libkvlinc.so")  # KVLC_LIB: tracing build
 
 KVLC_OK, KVLC_EINVAL, KVLC_ECUDA, KVLC_ENODEV, KVLC_ENOSPC = 0, 1, 2, 3, 4
 AXIS_TOKEN, AXIS_CHANNEL = 0, 1
