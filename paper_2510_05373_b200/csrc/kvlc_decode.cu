@@ -10,11 +10,12 @@
 // Kernels (one decode step = 2 launches, PDL-chained):
 //   phi_kernel      phi_q(q) per q-head and C_d = P . phi      (attention.py:224-228)
 //   split_kernel    per CTA task, selected by blockIdx:
-//                   * quantized split: chunks of one (b, kv-head) unit on the
-//                     tcgen05 tensor cores: bulk-TMA chunk ring, 2-bit codes
-//                     expanded into TMEM A operands (one LOP3 per two codes),
-//                     GQA heads on N, scales folded into the shared-memory B
-//                     operands, f32 accumulators in TMEM (kvlc_quant.cuh)
+//                   * quantized split: chunks of one (b, kv-head) unit, GQA
+//                     heads batched on the MMA N dimension, 2-bit codes turned
+//                     into fp16 MMA operands by one LOP3 each (exact subnormal
+//                     values c * 4^j * 2^-24), scales folded into q / p
+//                     (hi+lo fp16 split when the group has <= 4 heads)
+//                     (kvlc_quant.cuh)
 //                   * residual half: bf16 ring window, masked
 //                   * correction rows: C_n = S phi for 32 rows of S
 //                   the last CTA of each unit performs the LSE merge of the
@@ -24,7 +25,6 @@
 // Online-softmax state is kept in log2 units (logit * log2 e); the sign of the
 // global max, which selects the correction branch, is unit independent.
 #include "kvlc_common.cuh"
-#include "kvlc_tc.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -39,17 +39,24 @@ constexpr int SLOTS = KVLC_SLOTS;
 constexpr int RANK = KVLC_RANK;
 constexpr int HALF = RANK / 2;
 constexpr int WARPS = 4;
-constexpr int THREADS = WARPS * 32;   // residual / correction / combine CTAs
-constexpr int QTHREADS = 256;         // quantized-split CTAs (token + channel warps)
+constexpr int THREADS = WARPS * 32;
 constexpr int REC = 4 + D;  // record: m (log2 units), l, pad, pad, y[D] (16-byte aligned y)
 constexpr int PREC = 4 + 2 * D;  // device-partial record: m, l, pad, pad, y_rot[D], y_raw[D]
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float C0 = 0.12751743074173226f;  // log2(e) / sqrt(128)
-constexpr int CORR_ROWS = 64;               // S rows per correction task (8 per warp)
-constexpr int CORR_TASKS = D / CORR_ROWS;
-constexpr int TWARPS = 8;                   // warps of a persistent split CTA
+constexpr int CORR_ROWS = 32;               // S rows per correction CTA
+constexpr int CORR_CTAS = D / CORR_ROWS;
 
 __device__ __forceinline__ float bf2f(uint16_t x) { return __uint_as_float((uint32_t)x << 16); }
+
+__device__ __forceinline__ void mma_f16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                        uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 
 __device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -75,6 +82,22 @@ __device__ __forceinline__ uint4 ldg4(const void* p) {
 __device__ __forceinline__ uint2 ldg2(const void* p) {
   return __ldg(reinterpret_cast<const uint2*>(p));
 }
+__device__ __forceinline__ uint32_t w4(const uint4& v, int i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+// byte b of x into byte 0 and byte b of y into byte 2 (bytes 1, 3 are masked off later)
+__device__ __forceinline__ uint32_t pick(uint32_t x, uint32_t y, int b) {
+  return __byte_perm(x, y, (uint32_t)(b | (b << 4) | ((4 + b) << 8) | ((4 + b) << 12)));
+}
+// half2 of fp16 subnormals (c_lo * 4^j * 2^-24, c_hi * 4^j * 2^-24)
+__device__ __forceinline__ uint32_t code_h2(uint32_t x, int j) { return x & (0x00030003u << (2 * j)); }
+
+// 2^24 * 4^-j
+__device__ __forceinline__ constexpr float code_unscale(int j) {
+  return j == 0 ? 16777216.f : (j == 1 ? 4194304.f : (j == 2 ? 1048576.f : 262144.f));
+}
+
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n"); }
 
@@ -92,7 +115,6 @@ struct DecArgs {
   int nrec;               // records per unit = nsq + 2*tail
   // fused LSE combine: the last CTA of a unit merges its records
   uint32_t* done;         // [U] arrival counters (zeroed before the launch, self-cleaning)
-  uint32_t* queue;        // [2] work-item counter, exited-CTA counter (self-cleaning)
   int literal;
   int out_fp32;
   void* out;              // [B][Hq][D] bf16 / f32 (final output)
@@ -185,13 +207,13 @@ __global__ void __launch_bounds__(256) phi_kernel(kvlc_cache c, int NG, const fl
 
 #include "kvlc_quant.cuh"
 
-// Residual window: the 256 ring slots, 32 per warp, one record (index nsq).
+// Residual window half hf: ring slots [128 hf, 128 hf + 128), 32 per warp.
 __device__ __forceinline__ int res_sigma(int r) {  // QK row -> slot offset within a 16-slot tile
   return r < 8 ? 2 * r - (r & 1) : 2 * (r - 8) - ((r - 8) & 1) + 2;
 }
 
 template <int NG>
-__device__ void run_resid(const DecArgs& a, int unit, float* smrec) {
+__device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
   const kvlc_cache& c = a.c;
   constexpr bool HILO = NG <= 4;
   constexpr int NH = WarpState<NG>::NH;
@@ -199,7 +221,7 @@ __device__ void run_resid(const DecArgs& a, int unit, float* smrec) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int start = c.res_start[b], len = c.res_len[b];
-  const int base = 32 * warp;
+  const int base = 128 * hf + 32 * warp;
   WarpState<NG> st;
   st.init();
   auto live = [&](int slot) { return ((slot - start) & (SLOTS - 1)) < len; };
@@ -301,9 +323,9 @@ __device__ void run_resid(const DecArgs& a, int unit, float* smrec) {
       }
     }
   }
-  warp_store<NG>(st, smrec + warp * NG * REC, lane);
+  warp_store<NG, false>(st, smrec + warp * NG * REC, lane);
   __syncthreads();
-  cta_merge<NG, TWARPS>(smrec, a.rec + ((size_t)unit * a.nrec + a.nsq) * NG * REC);
+  cta_merge<NG>(smrec, a.rec + ((size_t)unit * a.nrec + a.nsq + hf) * NG * REC);
 }
 
 // C_n = S phi for CORR_ROWS rows of S (8 per warp).  Waits for phi_kernel.
@@ -322,23 +344,23 @@ __device__ void run_corr(const DecArgs& a, int unit, int rb) {
     ph[i][0] = x.x; ph[i][1] = x.y; ph[i][2] = x.z; ph[i][3] = x.w;
     ph[i][4] = y.x; ph[i][5] = y.y; ph[i][6] = y.z; ph[i][7] = y.w;
   }
-  const int row0 = rb * CORR_ROWS + warp * (CORR_ROWS / TWARPS);
-  float4 sr[CORR_ROWS / TWARPS][2];
+  const int row0 = rb * CORR_ROWS + warp * (CORR_ROWS / WARPS);
+  float4 sr[CORR_ROWS / WARPS][2];
 #pragma unroll
-  for (int r = 0; r < CORR_ROWS / TWARPS; ++r) {
+  for (int r = 0; r < CORR_ROWS / WARPS; ++r) {
     const float4* sp = reinterpret_cast<const float4*>(c.S + ((size_t)unit * D + row0 + r) * RANK + lane * 8);
     sr[r][0] = __ldg(sp);
     sr[r][1] = __ldg(sp + 1);
   }
   // per-lane partial dots for the warp's 8 rows x NG heads, then one
   // reduce-scatter per 32 values: lane L ends with the total of value L
-  constexpr int NV = (CORR_ROWS / TWARPS) * NG;
+  constexpr int NV = (CORR_ROWS / WARPS) * NG;
   constexpr int NB = (NV + 31) / 32;
   float vals[NB * 32];
 #pragma unroll
   for (int n = 0; n < NB * 32; ++n) vals[n] = 0.f;
 #pragma unroll
-  for (int r = 0; r < CORR_ROWS / TWARPS; ++r) {
+  for (int r = 0; r < CORR_ROWS / WARPS; ++r) {
     const float s8[8] = {sr[r][0].x, sr[r][0].y, sr[r][0].z, sr[r][0].w,
                          sr[r][1].x, sr[r][1].y, sr[r][1].z, sr[r][1].w};
 #pragma unroll
@@ -512,115 +534,44 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
   finish(M, Mt, den, nr, nw, corr ? cbuf : nullptr, a.literal, lane, o, a.out_fp32);
 }
 
-// The whole decode step's split-KV work in one persistent launch: 2 CTAs per
-// SM pull work items from a global counter in this order:
-//   [U * nsq quantized splits] [U residual windows] [U * CORR_TASKS correction
-//   row blocks] [U combines].
-// A CTA first runs one continuous chunk stream over the quantized splits it
-// pops (run_quant_stream), then the remaining items one by one.  Every
-// producing item publishes its record with a release add on its unit's
-// arrival counter; a combine item waits (acquire) for its unit's count, then
-// performs the LSE merge (no separate combine launch).  TMEM and the MMA
-// mbarriers are set up once per CTA.  Dynamic shared memory SPLIT_SMEM (> 1/3
-// of the SM) keeps at most two CTAs per SM, so the two 256-column TMEM
-// allocations always fit.
-constexpr size_t SPLIT_SMEM = 100 * 1024;
-static_assert(sizeof(TcSmem) + 1024 <= SPLIT_SMEM, "TcSmem exceeds the split kernel's shared memory");
-static_assert(TWARPS * 8 * REC * sizeof(float) <= SPLIT_SMEM, "residual records exceed shared memory");
-
-#ifdef KVLC_TRACE
-__device__ unsigned long long g_cta[4096][4];  // start ns, end ns, smid, task (1 resid, 2 corr, 3 combine)
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#endif
-
-template <int NG>
-__global__ void __launch_bounds__(QTHREADS, 2) split_kernel(const DecArgs a) {
-  extern __shared__ __align__(1024) unsigned char dsm[];
-  __shared__ int s_item;
-  TcSmem& sm = *reinterpret_cast<TcSmem*>(dsm);
+// The whole decode step's split-KV work in one launch; blockIdx selects the
+// task: quantized splits, residual halves, correction rows.  Every CTA bumps
+// its unit's arrival counter after publishing its record; the last one
+// performs the LSE combine of the unit (no separate combine launch).
+template <int NG, int EXTRA>
+__global__ void __launch_bounds__(THREADS, 4) split_kernel(const DecArgs a) {
+  __shared__ __align__(16) SplitSmem sm;
+  __shared__ int last;
   const int U = a.c.B * a.c.Hkv;
-  const int nq = U * a.nsq;
-  const int nres = a.tail ? U : 0, ncorr = a.tail && a.corr_on ? U * CORR_TASKS : 0;
-  const int nitems = nq + nres + ncorr + U;
-  const int per_unit = a.nsq + (a.tail ? 1 + (a.corr_on ? CORR_TASKS : 0) : 0);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) tc::tmem_alloc(&sm.tbase, TMEM_COLS);
-  if (tid == 0) {
-    tc::mbar_init(&sm.mqk, 1);
-    tc::mbar_init(&sm.mpv, 1);
-    tc::mbar_fence_init();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tb = sm.tbase;
-  uint32_t qk_ph = 0, pv_ph = 0;
-#ifdef KVLC_TRACE
-  const unsigned long long t_s0 = gtime();
-#endif
-  int it = run_quant_stream<NG>(a, nq, sm, tb, qk_ph, pv_ph);  // first non-quantized item popped
-#ifdef KVLC_TRACE
-  if (tid == 0 && blockIdx.x < 296) {
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_cta[3700 + blockIdx.x][0] = t_s0;
-    g_cta[3700 + blockIdx.x][1] = gtime();
-    g_cta[3700 + blockIdx.x][2] = smid;
-    g_cta[3700 + blockIdx.x][3] = 0;
-  }
-#endif
-  while (it < nitems) {
-#ifdef KVLC_TRACE
-    if (tid == 0 && it < 4096) {
-      uint32_t smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      g_cta[it][0] = gtime();
-      g_cta[it][2] = smid;
-      g_cta[it][3] = it - nq < nres ? 1 : (it - nq - nres < ncorr ? 2 : 3);
+  int x = blockIdx.x, unit;
+  if (x < U * a.nsq) {
+    unit = x / a.nsq;
+    run_quant<NG, EXTRA>(a, unit, x % a.nsq, sm);
+  } else {
+    x -= U * a.nsq;
+    if (x < 2 * U) {
+      unit = x / 2;
+      run_resid<NG>(a, unit, x % 2, sm.rec);
+    } else {
+      x -= 2 * U;
+      unit = x / CORR_CTAS;
+      run_corr<NG>(a, unit, x % CORR_CTAS);
     }
-#endif
-    int x = it - nq;
-    if (x < nres + ncorr) {
-      int unit;
-      if (x < nres) {
-        unit = x;
-        run_resid<NG>(a, unit, reinterpret_cast<float*>(dsm));
-      } else {
-        x -= nres;
-        unit = x / CORR_TASKS;
-        run_corr<NG>(a, unit, x % CORR_TASKS);
-      }
-      __syncthreads();
-      if (tid == 0) red_release_add(a.done + unit, 1u);  // publish this item's record / correction rows
-    } else {  // combine of unit x - nres - ncorr, once all its items are published
-      const int unit = x - nres - ncorr;
-      if (tid == 0)
-        while (ld_acquire(a.done + unit) < (uint32_t)per_unit) __nanosleep(128);
-      __syncthreads();
-      if (a.corr_on) griddep_wait();  // C_d comes from phi_kernel
-      const int b = unit / a.c.Hkv, kvh = unit % a.c.Hkv;
-      for (int h = warp; h < NG; h += TWARPS) combine_head(a, NG, b, h, kvh, lane);
-      if (tid == 0) a.done[unit] = 0u;  // self-cleaning for the next step
-    }
-#ifdef KVLC_TRACE
-    if (tid == 0 && it < 4096) g_cta[it][1] = gtime();
-#endif
-    __syncthreads();
-    if (tid == 0) s_item = (int)atomicAdd(a.queue, 1u);
-    __syncthreads();
-    it = s_item;
   }
-  tc::fence_before_sync();
+  const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? CORR_CTAS : 0) : 0);
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tb, TMEM_COLS);
-  if (tid == 0 && atomicAdd(a.queue + 1, 1u) == gridDim.x - 1) {  // last CTA out resets the queue
-    a.queue[0] = 0u;
-    a.queue[1] = 0u;
+  if (threadIdx.x == 0) {
+    __threadfence();  // publish this CTA's record / correction rows
+    last = atomicAdd(a.done + unit, 1u) == (uint32_t)(per_unit - 1);
   }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (a.corr_on) griddep_wait();  // C_d comes from phi_kernel
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = unit / a.c.Hkv, kvh = unit % a.c.Hkv;
+  for (int h = warp; h < NG; h += WARPS) combine_head(a, NG, b, h, kvh, lane);
+  if (threadIdx.x == 0) a.done[unit] = 0u;  // self-cleaning for the next step
 }
 
 // LSE merge of n device records (m, l, y_rot, y_raw) + correction -> out.
@@ -663,15 +614,6 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
 }
 
 // ------------------------------------------------------------- host ----
-int persistent_ctas() {  // 2 resident split CTAs per SM
-  static int n = [] {
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return 2 * sms;
-  }();
-  return n;
-}
-
 struct Plan {
   int NG, U, nsq, cpc, nrec, corr_on;
   size_t done_off, phi_off, corr_off, rec_off, total;
@@ -687,14 +629,15 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   int span = std::max(0, std::min(maxc, chunk_hi) - chunk_lo);
   int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : 0;
   if (cpc == 0) {
-    // ~3 quantized items per persistent CTA (dynamic balance), at least 4 chunks each
-    const int pieces = std::max(1, (3 * persistent_ctas() + p.U - 1) / p.U);
-    cpc = std::max(4, std::min(MAX_CPC, (std::max(span, 1) + pieces - 1) / pieces));
+    // ~2 waves of quantized-split CTAs at 4 resident CTAs per SM
+    const long long ctas_wanted = 148LL * 4 * 2;
+    const long long chunks = (long long)p.U * std::max(span, 1);
+    cpc = (int)std::max(2LL, std::min(32LL, (chunks + ctas_wanted - 1) / ctas_wanted));
   }
   p.cpc = cpc;
   p.nsq = std::max(1, (span + cpc - 1) / cpc);
   p.corr_on = corr_on && tail ? 1 : 0;
-  p.nrec = p.nsq + (tail ? 1 : 0);
+  p.nrec = p.nsq + (tail ? 2 : 0);
   size_t BH = (size_t)c->B * c->Hq;
   p.phi_off = 0;
   p.corr_off = align_up(BH * RANK * sizeof(float));
@@ -702,7 +645,7 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   // arrival counters first: their offset must not depend on the split plan
   // (they are zero-initialised once and left at zero by every launch)
   p.done_off = 0;
-  const size_t base = align_up((size_t)(p.U + 2) * sizeof(uint32_t));  // done[U], queue[2]
+  const size_t base = align_up((size_t)p.U * sizeof(uint32_t));
   p.phi_off += base;
   p.corr_off += base;
   p.rec_off += base;
@@ -737,18 +680,17 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   a.corr_on = p.corr_on;
   a.nrec = p.nrec;
   a.done = reinterpret_cast<uint32_t*>(ws + p.done_off);
-  a.queue = a.done + p.U;
   a.literal = literal;
   a.out_fp32 = out_fp32;
   a.out = out;
   a.rec_out = rec_out;
-  int grid = persistent_ctas();
+  int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? p.U * CORR_CTAS : 0) : 0);
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(QTHREADS);
+  cfg.blockDim = dim3(THREADS);
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = p.corr_on ? 1 : 0;
@@ -756,9 +698,21 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_begin), s));
     cfg.numAttrs = 0;  // the event already orders the launch
   }
-  cfg.dynamicSmemBytes = SPLIT_SMEM;
-  KVLC_CUDA(cudaFuncSetAttribute(split_kernel<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SPLIT_SMEM));
-  KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG>, a));
+  if (NG <= 4) {
+    KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a));
+  } else {
+    // precision passes for > 4 heads per group (see quant_chunk); KVLC_EXTRA overrides (tuning)
+    static const int extra = [] {
+      const char* e = getenv("KVLC_EXTRA");
+      return e ? atoi(e) & 3 : 3;
+    }();
+    switch (extra) {
+      case 0: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a)); break;
+      case 1: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 1>, a)); break;
+      case 2: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 2>, a)); break;
+      default: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 3>, a)); break;
+    }
+  }
   if (o && o->ev_end) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_end), s));
   return check_launch("decode");
 }
@@ -830,17 +784,6 @@ int kvlc_decode_partial(const kvlc_cache* c, const kvlc_adapter* ad, const uint1
   return launch(c, ad, q, p, static_cast<char*>(ws), chunk_lo, chunk_hi, include_tail ? 1 : 0, corr,
                 0, 0, nullptr, rec, o, as_stream(stream));
 }
-
-#ifdef KVLC_TRACE
-int kvlc_debug_trace(void* dst, size_t bytes) {
-  KVLC_CUDA(cudaMemcpyFromSymbol(dst, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace)));
-  return KVLC_OK;
-}
-int kvlc_debug_cta(void* dst, size_t bytes) {
-  KVLC_CUDA(cudaMemcpyFromSymbol(dst, g_cta, bytes < sizeof(g_cta) ? bytes : sizeof(g_cta)));
-  return KVLC_OK;
-}
-#endif
 
 int kvlc_merge_records(const float* recs, int32_t n_rec, int64_t rec_stride, const float* corr,
                        int32_t B, int32_t Hq, int32_t literal, int32_t out_fp32, void* out,

@@ -50,47 +50,49 @@ __device__ __forceinline__ bool near_half_tie(double x) {
          __half_as_ushort(__double2half(x * (1.0 + 1e-12)));
 }
 
-// ---- row-native code layouts (include/kvlinc.h, consumed by kvlc_quant.cuh) ----
-// A chunk's K codes are 128 token rows of 8 words, its V codes 128 channel rows
-// of 8 words.  Byte b, bit pair p of logical word w of a row holds element
-//   e = 2 * (8w + 4(b & 1) + p) + (b >> 1)
-// (a channel for K rows, a token for V rows), so that `word & (0x00030003 << 2p)`
-// (and the same on word >> 8) is the fp16 pair of elements (2j, 2j+1),
-// j = 8w + 4(b & 1) + p, as exact subnormals c * 4^p * 2^-24: TMEM column j
-// of the MMA A operand.  The two 16-B halves of a row are swapped on rows with
-// (row >> 2) & 1 (bank-conflict-free LDS.128): logical word w of row r sits
-// at position w ^ (4 * ((r >> 2) & 1)).
-__device__ __forceinline__ int row_elem(int w, int b, int p) { return 2 * (8 * w + 4 * (b & 1) + p) + (b >> 1); }
-__device__ __forceinline__ int row_pos(int r, int w) { return w ^ (((r >> 2) & 1) << 2); }
-
-// word at position wi (= row * 8 + pos) of a chunk; codes [token][channel]
+// ---- fragment-native code layouts (include/kvlinc.h, consumed by kvlc_decode.cu) ----
+// Key word wi = ((w*32 + lane)*8 + kt), lane = 4g + t0: byte q holds channel
+// 16kt + 2t0 + {0,8,1,9}[q]; its bit pair j holds token 32w + 4g + j.
 __device__ __forceinline__ uint32_t pack_k_word(const uint8_t* codes, int wi) {
-  const int r = wi >> 3, w = row_pos(r, wi & 7);
+  const int kt = wi & 7, lane = (wi >> 3) & 31, w = wi >> 8;
+  const int g = lane >> 2, t0 = lane & 3;
+  const int coff[4] = {0, 8, 1, 9};
   uint32_t word = 0;
 #pragma unroll
-  for (int b = 0; b < 4; ++b)
+  for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int p = 0; p < 4; ++p) word |= (uint32_t)codes[r * D + row_elem(w, b, p)] << (8 * b + 2 * p);
+    for (int j = 0; j < 4; ++j)
+      word |= (uint32_t)codes[(32 * w + 4 * g + j) * D + 16 * kt + 2 * t0 + coff[q]] << (8 * q + 2 * j);
   return word;
 }
 
+// Value word wi = ((w*32 + lane)*8 + 4mt + p), lane = 4g + t0: byte q holds
+// token 32w + 8t0 + 2mt + {0,1,4,5}[q]; its bit pair j holds channel 32p + 8j + g.
 __device__ __forceinline__ uint32_t pack_v_word(const uint8_t* codes, int wi) {
-  const int r = wi >> 3, w = row_pos(r, wi & 7);
+  const int i = wi & 7, lane = (wi >> 3) & 31, w = wi >> 8;
+  const int g = lane >> 2, t0 = lane & 3, mt = i >> 2, p = i & 3;
+  const int toff[4] = {0, 1, 4, 5};
   uint32_t word = 0;
 #pragma unroll
-  for (int b = 0; b < 4; ++b)
+  for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int p = 0; p < 4; ++p) word |= (uint32_t)codes[row_elem(w, b, p) * D + r] << (8 * b + 2 * p);
+    for (int j = 0; j < 4; ++j)
+      word |= (uint32_t)codes[(32 * w + 8 * t0 + 2 * mt + toff[q]) * D + 32 * p + 8 * j + g] << (8 * q + 2 * j);
   return word;
 }
 
-// Code of element e of row r (inverse of row_elem / row_pos).
-__device__ __forceinline__ uint32_t row_code(const uint32_t* words, int r, int e) {
-  const int j = e >> 1, w = j >> 3, b = ((j >> 2) & 1) + 2 * (e & 1), p = j & 3;
-  return (words[r * 8 + row_pos(r, w)] >> (8 * b + 2 * p)) & 3u;
+// Code of (token t, channel c) of one chunk, from the device layouts above.
+__device__ __forceinline__ uint32_t k_code(const uint32_t* words, int t, int c) {
+  const int w = t >> 5, u = t & 31, g = u >> 2, j = u & 3;
+  const int kt = c >> 4, cc = c & 15, t0 = (cc & 7) >> 1, q = ((cc & 1) << 1) | (cc >> 3);
+  return (words[((w * 32) + 4 * g + t0) * 8 + kt] >> (8 * q + 2 * j)) & 3u;
 }
-__device__ __forceinline__ uint32_t k_code(const uint32_t* words, int t, int c) { return row_code(words, t, c); }
-__device__ __forceinline__ uint32_t v_code(const uint32_t* words, int t, int c) { return row_code(words, c, t); }
+
+__device__ __forceinline__ uint32_t v_code(const uint32_t* words, int t, int c) {
+  const int w = t >> 5, u = t & 31, t0 = u >> 3, hi = (u >> 2) & 1, mt = (u >> 1) & 1, lo = u & 1;
+  const int q = lo + 2 * hi, g = c & 7, r = (c >> 3) & 1, mv = c >> 4, p = mv >> 1, j = 2 * (mv & 1) + r;
+  return (words[((w * 32) + 4 * g + t0) * 8 + 4 * mt + p] >> (8 * q + 2 * j)) & 3u;
+}
 
 constexpr int MAX_B = 1024;
 

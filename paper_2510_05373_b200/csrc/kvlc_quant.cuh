@@ -1,90 +1,30 @@
-// Quantized-split path of the fused decode (included by kvlc_decode.cu), on
-// the 5th-generation tensor cores (tcgen05, TMEM accumulators, bulk TMA).
+// Quantized-split path of the fused decode (included by kvlc_decode.cu).
 //
-// A quantized-split CTA (4 warps, thread i) owns chunks [lo, hi) of one
-// (b, kv-head) unit.  Per 128-token chunk:
-//   * one elected thread streams the chunk (K codes 4 KB, V codes 4 KB, the
-//     four 256-B fp16 scale / zero vectors) into an NSTAGE-deep shared-memory
-//     ring with cp.async.bulk (TMA), completion on an mbarrier;
-//   * thread i expands token i's K row and channel i's V row (2-bit codes ->
-//     fp16 pairs, one LOP3 per two codes: the exact subnormals c*4^p*2^-24 of
-//     the row-native layout written by kvlc_flush.cu) and stores them into
-//     TMEM with tcgen05.st — TMEM lane i is row i of the MMA A operand;
-//   * the small B operands live in shared memory: B_QK[c] = q*s_k[c]*4^-p(c)
-//     (fp16 hi + lo columns per GQA head; the 4^-p undoes the code's bit-pair
-//     weight) and, after the softmax, B_PV[t] = p_t*s_v[t]*4^-p(t); the zero
-//     terms q . z_k (keys) and sum_t p_t z_v[t] (values) are per-head scalars
-//     computed in fp32;
-//   * MMAs are kind::f16, M = 128, N = 16, K = 16 with f32 accumulators in
-//     TMEM: D_QK = A_K B_QK (logits), D_PV = A_V B_PV (numerator);
-//   * the online softmax keeps one CTA-wide reference point per head (log2
-//     units) that moves only when a logit exceeds it by LAZY (rare); each
-//     chunk's PV result is drained from TMEM into fp32 registers (the tensor
-//     core's f32 accumulation is not carried across chunks).
-// Roles and pipeline: see run_quant below.
-// Reference: the per-block loop of decode_step_blocked (attention.py:238-247)
-// with the block partial (m, l, y) of DecodePartial (attention.py:41-47).
+// A quantized-split CTA owns chunks [lo, hi) of one (b, kv-head) unit.  Its
+// 4 warps take the 4 32-token slices of every chunk:
+//   * each warp streams its slice (1 KB of K codes, 1 KB of V codes, the
+//     slice's V scale/zero and the K scale/zero of its B-operand share)
+//     through a 3-stage cp.async pipeline in shared memory;
+//   * the QK^T B operand of a chunk (q' = q * s_k, fp16 hi/lo) and the zero
+//     term zt = q . z_k are built cooperatively (warp w: k-tiles 2w, 2w+1),
+//     double-buffered in shared memory, one CTA barrier per chunk;
+//   * codes become fp16 MMA operands with one LOP3 per register (exact
+//     subnormals c * 4^j * 2^-24 from the fragment-native layouts written by
+//     kvlc_flush.cu); mma.sync m16n8k16, GQA heads on N;
+//   * online softmax in log2 units with lazy rescaling: the reference point
+//     only moves when the running max grows by more than LAZY (p <= 2^LAZY),
+//     the true max is tracked separately for literal-correction parity.
 #pragma once
 
+constexpr int STAGES = 3;
+constexpr float LAZY = 8.f;
 
-
-constexpr float LAZY = 6.f;          // reference point moves when p would exceed 2^LAZY
-constexpr int NSTAGE = 5;            // chunk ring depth (cp.async lookahead NSTAGE - 2 chunks)
-constexpr int MAX_CPC = 64;          // chunks per quantized split (plan_for caps cpc)
-constexpr int IFIFO = 8;             // quantized items in flight per CTA (> NSTAGE + 1)
-constexpr float QK_SCALE = 256.f;    // B_QK / B_Z prescale (fp16 range use), undone on readback
-
-// TMEM columns (256 allocated per CTA; 2 quantized CTAs per SM)
-constexpr uint32_t COL_AK = 0;      // A_K x2 [128 tokens][128 channels] fp16 pairs: 2 x 64 columns
-constexpr uint32_t COL_AV = 128;    // A_V    [128 channels][128 tokens]: 64 columns
-constexpr uint32_t COL_DQK = 192;   // D_QK   [128 tokens][16] f32
-constexpr uint32_t COL_DPV = 208;   // D_PV   [128 channels][16] f32
-constexpr uint32_t COL_ONES = 224;  // A_ones [128][16] fp16 2^-24 (key zero term): 8 columns
-constexpr uint32_t TMEM_COLS = 256;
-
-__device__ __forceinline__ float fast_exp2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
-  return y;
-}
-
-struct ChunkStage {
-  uint4 kc[256];    // K codes: token row r = words 0-3 at uint4 2r + sw(r), words 4-7 at 2r + 1 - sw(r)
-  uint4 vc[256];    // V codes: channel row, same swizzle
-  uint16_t ks[128], kz[128];  // per channel
-  uint16_t vs[128], vz[128];  // per token
-};
-
-struct QItem {
-  int unit, split, n;  // chunks [chunk_lo + split * cpc, + n) of unit
-};
-
-struct TcSmem {
-  ChunkStage stage[NSTAGE];
-  uint4 bqk[2][256];  // [128 rows][16 cols] fp16 MN-major: cols 0-7 at uint4 r, cols 8-15 at 128 + r
-  uint4 bz[2][256];   // key zero-term rows (q z_k), same layout
-  uint4 bpv[2][256];  // double-buffered: the MMA of chunk k-1 may still read the other one
-  float ob[2][8];     // reference point of chunk k's B_PV [k & 1][head]
-  float red[4][8][4];
-  float itred[2][4][8][4];  // per-item token-warp totals (l, sum p z_v, true max) [item & 1][warp][head]
-  QItem items[IFIFO];       // quantized items of this CTA's chunk stream (FIFO, index & (IFIFO - 1))
-  uint16_t qv[IFIFO][8][128];  // their query vectors (bf16, staged by the loaders with cp.async)
-  int n_items;              // items popped into the FIFO
-  int empty_unit, empty_split;  // loader scratch: a popped item without chunks
-  int loaded;               // stream chunks issued into the ring
-  int end;                  // stream length once the loaders reached the end of the quantized items
-  int next;                 // first non-quantized work item popped by the loaders
-  uint64_t mqk, mpv;
-  uint32_t tbase;
-};
-
-// Residual-window warp state (kvlc_decode.cu run_resid): mma.sync bf16 path.
 template <int NG>
 struct WarpState {
   static constexpr bool HILO = NG <= 4;
   static constexpr int NH = HILO ? 1 : 2;
-  float m[NH];   // reference point of p (log2 units)
-  float mt[NH];  // true running max
+  float m[NH];      // reference point of p (log2 units)
+  float mt[NH];     // true running max
   float l[NH], z[NH];
   float acc[8][4];
   __device__ __forceinline__ void init() {
@@ -102,18 +42,292 @@ struct WarpState {
   }
 };
 
-// Writes a residual warp's record (m_ref, l, m_true, -, y[c]) per head into shared memory.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// One warp's data for one chunk.
+struct WarpStage {
+  uint4 k[2][32];   // K words 0-3 / 4-7 of each lane (fragment-native layout)
+  uint4 v[2][32];   // V words
+  uint2 vs[8];      // V scales of tokens 32w + 4g .. +3, per g
+  uint2 vz[8];
+  uint2 ks[8];      // K scales of channels 32w .. 32w+31 (the warp's B share)
+  uint2 kz[8];
+};
+
+struct QuantSmem {
+  WarpStage stage[STAGES][WARPS];
+  uint4 bq[2][4][32];   // [buf][k-tile pair][lane]: (b0, b1 of kt = 2p, b0, b1 of kt = 2p+1)
+  uint4 bl[2][4][32];   // low parts (groups of > 4 heads)
+  float4 zt[2][8];      // [buf][column g] -> partial zero terms of the 4 warps
+};
+
+union SplitSmem {
+  QuantSmem quant;
+  float rec[WARPS * 8 * REC];
+};
+
+// Per-lane source pointers of a warp's slice; every lane issues the same
+// cp.async sequence (2 x 16 B K, 2 x 16 B V, one 8 B metadata piece: lanes
+// 0-7 V scales, 8-15 V zeros, 16-23 K scales, 24-31 K zeros).  All sources
+// advance by a fixed stride per chunk.
+struct SliceSrc {
+  const uint4* k;     // advances 256 uint4 (4 KB) per chunk
+  const uint4* v;
+  const uint2* meta;  // advances 32 uint2 (256 B) per chunk
+  __device__ __forceinline__ void init(const kvlc_cache& c, size_t cb, int warp, int lane) {
+    k = reinterpret_cast<const uint4*>(c.kcodes + ((cb * 4 + warp) * 32 + lane) * 8);
+    v = reinterpret_cast<const uint4*>(c.vcodes + ((cb * 4 + warp) * 32 + lane) * 8);
+    const int role = lane >> 3, sub = lane & 7;
+    const uint16_t* base = role == 0 ? c.vscale : role == 1 ? c.vzero : role == 2 ? c.kscale : c.kzero;
+    meta = reinterpret_cast<const uint2*>(base + cb * 128 + 32 * warp + 4 * sub);
+  }
+  __device__ __forceinline__ void issue(WarpStage& st, int lane, int chunk_off) const {
+    const uint4* kp = k + (size_t)chunk_off * 256;
+    const uint4* vp = v + (size_t)chunk_off * 256;
+    cp_async16(&st.k[0][lane], kp);
+    cp_async16(&st.k[1][lane], kp + 1);
+    cp_async16(&st.v[0][lane], vp);
+    cp_async16(&st.v[1][lane], vp + 1);
+    cp_async8(&st.vs[0] + lane, meta + (size_t)chunk_off * 32);   // vs, vz, ks, kz are contiguous
+  }
+};
+
+// Builds this warp's share (k-tiles 2w, 2w+1) of a chunk's B operand from its stage.
+//  HILO: column n = g holds head g>>1: the hi part for even g, the lo part
+//        (exact FMA residual q*s - hi) for odd g.
+//  else: column n = g holds head g (hi in bq, lo in bl).
 template <int NG>
+__device__ __forceinline__ void build_b(QuantSmem& sm, int buf, const WarpStage& st,
+                                        const uint32_t (&qs)[4], int warp, int lane) {
+  constexpr bool HILO = NG <= 4;
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t* ks = reinterpret_cast<const uint32_t*>(st.ks);
+  const uint32_t* kz = reinterpret_cast<const uint32_t*>(st.kz);
+  uint32_t b[4], bl[4];
+  float zp = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    // i = 2e + k: channels 32w + 16e + 2t + {0,1} (+8 for k = 1)
+    const int pair = 8 * (i >> 1) + t + 4 * (i & 1);
+    const __half2 qv = u2h(qs[i]), sv = u2h(ks[pair]);
+    const __half2 hi = __hmul2(qv, sv);
+    if (HILO) {
+      const uint32_t neg = (g & 1) ? (h2u(hi) ^ 0x80008000u) : 0u;
+      b[i] = h2u(__hfma2(qv, sv, u2h(neg)));
+    } else {
+      b[i] = h2u(hi);
+      bl[i] = h2u(__hfma2(qv, sv, __hneg2(hi)));
+    }
+    const float2 qf = __half22float2(qv), zf = __half22float2(u2h(kz[pair]));
+    zp = fmaf(qf.x, zf.x, zp);
+    zp = fmaf(qf.y, zf.y, zp);
+  }
+  sm.bq[buf][warp][lane] = make_uint4(b[0], b[1], b[2], b[3]);
+  if (!HILO) sm.bl[buf][warp][lane] = make_uint4(bl[0], bl[1], bl[2], bl[3]);
+  zp += __shfl_xor_sync(0xffffffffu, zp, 1);
+  zp += __shfl_xor_sync(0xffffffffu, zp, 2);
+  if (t == 0) reinterpret_cast<float*>(&sm.zt[buf][g])[warp] = zp;
+}
+
+// One 128-token chunk, this warp's 32-token slice (tokens 32w .. 32w+31).
+// K word kt of lane (g, t) holds channels 16kt+2t+{0,8,1,9} in bytes 0..3 and
+// tokens 32w+4g+j at bits 2j; V word 4mt+p holds tokens 32w+8t+2mt+{0,1,4,5}
+// in bytes 0..3 and channels 32p+8j+g at bits 2j.
+template <int NG, int EXTRA>
+__device__ __forceinline__ void quant_chunk(const WarpStage& stg, const QuantSmem& sm, int buf,
+                                            WarpState<NG>& st, int lane) {
+  constexpr bool HILO = NG <= 4;
+  constexpr int NH = WarpState<NG>::NH;
+  constexpr bool QK_LO = !HILO && (EXTRA & 1);
+  constexpr bool PV_LO = !HILO && (EXTRA & 2);
+  const int g = lane >> 2, t = lane & 3;
+
+  float zt[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) {
+    const float4 zz = sm.zt[buf][HILO ? 2 * t : 2 * t + e];
+    zt[e] = ((zz.x + zz.y) + (zz.z + zz.w)) * C0;
+  }
+
+  // ---- Q K^T over the slice's 2 token tiles ----
+  float cq[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cq[i][j] = 0.f;
+  {
+    const uint4 k0 = stg.k[0][lane], k1 = stg.k[1][lane];
+    const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint4 b = sm.bq[buf][p][lane];
+      uint4 bl = make_uint4(0u, 0u, 0u, 0u);
+      if (QK_LO) bl = sm.bl[buf][p][lane];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const uint32_t x = kw[2 * p + e], y = x >> 8;
+        const uint32_t b0 = e ? b.z : b.x, b1 = e ? b.w : b.y;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const uint32_t a0 = code_h2(x, 2 * mt), a1 = code_h2(x, 2 * mt + 1);
+          const uint32_t a2 = code_h2(y, 2 * mt), a3 = code_h2(y, 2 * mt + 1);
+          mma_f16(cq[mt], a0, a1, a2, a3, b0, b1);
+          if (QK_LO) mma_f16(cq[mt], a0, a1, a2, a3, e ? bl.z : bl.x, e ? bl.w : bl.y);
+        }
+      }
+    }
+  }
+
+  // ---- online softmax: thread holds tokens 32w + 4g + (2mt + r) ----
+  float cmax[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) cmax[e] = -INFINITY;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float F = code_unscale(2 * mt + r) * C0;
+      if (HILO) {
+        const float v = fmaf(cq[mt][2 * r] + cq[mt][2 * r + 1], F, zt[0]);
+        cq[mt][2 * r] = v;
+        cmax[0] = fmaxf(cmax[0], v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const float v = fmaf(cq[mt][2 * r + e], F, zt[e]);
+          cq[mt][2 * r + e] = v;
+          cmax[e] = fmaxf(cmax[e], v);
+        }
+      }
+    }
+  }
+  bool grow = false;
+  float mref[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) {
+    float m = cmax[e];
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+    st.mt[e] = fmaxf(st.mt[e], m);
+    // move the reference point only when p would exceed 2^LAZY
+    mref[e] = m > st.m[e] + LAZY ? m : st.m[e];
+    grow |= mref[e] != st.m[e];
+  }
+  if (__any_sync(0xffffffffu, grow)) {
+    float sc[NH];
+#pragma unroll
+    for (int e = 0; e < NH; ++e) {
+      sc[e] = fast_exp2(st.m[e] - mref[e]);   // exp2(-inf) = 0 on the first chunk
+      st.m[e] = mref[e];
+      st.l[e] *= sc[e];
+      st.z[e] *= sc[e];
+    }
+#pragma unroll
+    for (int mv = 0; mv < 8; ++mv) {
+      if (HILO) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) st.acc[mv][j] *= sc[0];
+      } else {
+        st.acc[mv][0] *= sc[0];
+        st.acc[mv][2] *= sc[0];
+        st.acc[mv][1] *= sc[1];
+        st.acc[mv][3] *= sc[1];
+      }
+    }
+  }
+  const uint2 vs = stg.vs[g], vz = stg.vz[g];
+  const float2 s01 = __half22float2(u2h(vs.x)), s23 = __half22float2(u2h(vs.y));
+  const float2 z01 = __half22float2(u2h(vz.x)), z23 = __half22float2(u2h(vz.y));
+  const float svs[4] = {s01.x, s01.y, s23.x, s23.y}, svz[4] = {z01.x, z01.y, z23.x, z23.y};
+  uint32_t bp[2][2], bpl[2][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float sv = svs[2 * mt + r], zv = svz[2 * mt + r];
+      if (HILO) {
+        const float p = fast_exp2(cq[mt][2 * r] - st.m[0]);
+        st.l[0] += p;
+        st.z[0] = fmaf(p, zv, st.z[0]);
+        const float pv = p * sv;
+        // hi: pv truncated to 11 significant bits (fp16-exact), lo: the exact remainder
+        const float hi = __uint_as_float(__float_as_uint(pv) & 0xffffe000u);
+        bp[mt][r] = movm_t(h2u(__floats2half2_rn(hi, pv - hi)));
+      } else {
+        const float p0 = fast_exp2(cq[mt][2 * r] - st.m[0]);
+        const float p1 = fast_exp2(cq[mt][2 * r + 1] - st.m[1]);
+        st.l[0] += p0;
+        st.l[1] += p1;
+        st.z[0] = fmaf(p0, zv, st.z[0]);
+        st.z[1] = fmaf(p1, zv, st.z[1]);
+        const float a0 = p0 * sv, a1 = p1 * sv;
+        const __half2 hh = __floats2half2_rn(a0, a1);
+        bp[mt][r] = movm_t(h2u(hh));
+        if (PV_LO) {
+          const float2 hf = __half22float2(hh);
+          bpl[mt][r] = movm_t(h2u(__floats2half2_rn(a0 - hf.x, a1 - hf.y)));
+        }
+      }
+    }
+  }
+
+  // ---- P V: 8 channel tiles x the slice's 2 token tiles ----
+  const uint4 v0 = stg.v[0][lane], v1 = stg.v[1][lane];
+  const uint32_t vw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const uint32_t x = vw[4 * mt + p], y = x >> 8;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int mv = 2 * p + h;
+        const uint32_t a0 = code_h2(x, 2 * h), a1 = code_h2(x, 2 * h + 1);
+        const uint32_t a2 = code_h2(y, 2 * h), a3 = code_h2(y, 2 * h + 1);
+        mma_f16(st.acc[mv], a0, a1, a2, a3, bp[mt][0], bp[mt][1]);
+        if (PV_LO) mma_f16(st.acc[mv], a0, a1, a2, a3, bpl[mt][0], bpl[mt][1]);
+      }
+    }
+  }
+}
+
+// Writes this warp's record (m_ref, l, m_true, -, y[c]) per head into shared memory.
+// Quantized rows: channel 16mv + g + 8r with factor 2^24 4^-(2(mv&1)+r), plus
+// the value zero term; residual rows: channel 16mv + g + 8r, no factor.
+template <int NG, bool QUANT>
 __device__ __forceinline__ void warp_store(WarpState<NG>& st, float* smrec, int lane) {
   constexpr bool HILO = NG <= 4;
   constexpr int NH = WarpState<NG>::NH;
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int e = 0; e < NH; ++e) {
-    float l = st.l[e];
+    float l = st.l[e], z = st.z[e];
 #pragma unroll
-    for (int o = 4; o < 32; o <<= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    for (int o = 4; o < 32; o <<= 1) {
+      l += __shfl_xor_sync(0xffffffffu, l, o);
+      z += __shfl_xor_sync(0xffffffffu, z, o);
+    }
     st.l[e] = l;
+    st.z[e] = z;
   }
 #pragma unroll
   for (int e = 0; e < NH; ++e) {
@@ -126,29 +340,33 @@ __device__ __forceinline__ void warp_store(WarpState<NG>& st, float* smrec, int 
       r[2] = st.mt[e];
     }
 #pragma unroll
-    for (int mv = 0; mv < 8; ++mv)
+    for (int mv = 0; mv < 8; ++mv) {
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
-        r[4 + 16 * mv + g + 8 * rr] = HILO ? st.acc[mv][2 * rr] + st.acc[mv][2 * rr + 1] : st.acc[mv][2 * rr + e];
+      for (int rr = 0; rr < 2; ++rr) {
+        float v = HILO ? st.acc[mv][2 * rr] + st.acc[mv][2 * rr + 1] : st.acc[mv][2 * rr + e];
+        if (QUANT) v = fmaf(v, code_unscale(2 * (mv & 1) + rr), st.z[e]);
+        r[4 + 16 * mv + g + 8 * rr] = v;
+      }
+    }
   }
 }
 
 // Merges the WARPS per-warp records in shared memory into one global record per head.
 // (the caller has synchronised after warp_store)
-template <int NG, int NW>
+template <int NG>
 __device__ __forceinline__ void cta_merge(float* sm, float* out) {
-  __shared__ float wts[NG][NW];
+  __shared__ float wts[NG][WARPS];
   __shared__ float hdr[NG][4];
   if (threadIdx.x < NG) {
     const int h = threadIdx.x;
     float M = -INFINITY, Mt = -INFINITY, l = 0.f;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
+    for (int w = 0; w < WARPS; ++w) {
       M = fmaxf(M, sm[(w * NG + h) * REC]);
       Mt = fmaxf(Mt, sm[(w * NG + h) * REC + 2]);
     }
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
+    for (int w = 0; w < WARPS; ++w) {
       const float mw = sm[(w * NG + h) * REC];
       const float wt = mw == -INFINITY ? 0.f : exp2f(mw - M);
       wts[h][w] = wt;
@@ -160,7 +378,7 @@ __device__ __forceinline__ void cta_merge(float* sm, float* out) {
     hdr[h][3] = 0.f;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < NG * (D / 4 + 1); i += blockDim.x) {
+  for (int i = threadIdx.x; i < NG * (D / 4 + 1); i += THREADS) {
     const int h = i / (D / 4 + 1), k4 = i % (D / 4 + 1);
     float4 v;
     if (k4 == 0) {
@@ -168,7 +386,7 @@ __device__ __forceinline__ void cta_merge(float* sm, float* out) {
     } else {
       v = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int w = 0; w < NW; ++w) {
+      for (int w = 0; w < WARPS; ++w) {
         const float wt = wts[h][w];
         const float4 y = reinterpret_cast<const float4*>(sm + (w * NG + h) * REC)[k4];
         v.x = fmaf(wt, y.x, v.x);
@@ -181,522 +399,70 @@ __device__ __forceinline__ void cta_merge(float* sm, float* out) {
   }
 }
 
-// ------------------------------------------------------------ tcgen05 path --
-
-// 2-bit row (8 packed words) -> 64 fp16-pair registers -> TMEM columns [col, col+64)
-// of this thread's lane.  Column j = 8w + 4r + p holds the bit pair p of bytes
-// r (low half) and r + 2 (high half) of word w.
-__device__ __forceinline__ void expand4(const uint4& w, uint32_t* r) {
-  const uint32_t x[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t y = x[i] >> 8;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      r[8 * i + p] = x[i] & (0x00030003u << (2 * p));
-      r[8 * i + 4 + p] = y & (0x00030003u << (2 * p));
-    }
-  }
-}
-__device__ __forceinline__ void expand_row(const uint4* rows, int row, uint32_t taddr) {
-  const int sw = (row >> 2) & 1;  // 16-B halves swapped on alternate 4-row groups: conflict-free LDS.128
-  const uint4 w0 = rows[2 * row + sw], w1 = rows[2 * row + (sw ^ 1)];
-  uint32_t r[32];
-  expand4(w0, r);
-  kvlc::tc::tmem_st32(taddr, r);
-  expand4(w1, r);
-  kvlc::tc::tmem_st32(taddr + 32, r);
-}
-
-__device__ __forceinline__ uint32_t f2h2(float a, float b) {
-  __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
-
-// Row r of an N = 16 B tile: head h's fp16 hi part at column h, lo part
-// (exact remainder, rounded) at column LO + h (LO = 4 for <= 4 heads, else 8).
-template <int NG>
-__device__ __forceinline__ void write_brow(uint4* tile, int r, const float* x) {
-  constexpr int NP = NG <= 4 ? 4 : 8;
-  float v[NP], lo[NP];
-#pragma unroll
-  for (int h = 0; h < NP; ++h) v[h] = h < NG ? x[h] : 0.f;
-  uint32_t hi2[NP / 2], lo2[NP / 2];
-#pragma unroll
-  for (int i = 0; i < NP / 2; ++i) {
-    hi2[i] = f2h2(v[2 * i], v[2 * i + 1]);
-    const float2 hf = __half22float2(*reinterpret_cast<__half2*>(&hi2[i]));
-    lo[2 * i] = v[2 * i] - hf.x;
-    lo[2 * i + 1] = v[2 * i + 1] - hf.y;
-    lo2[i] = f2h2(lo[2 * i], lo[2 * i + 1]);
-  }
-  if constexpr (NG <= 4) {
-    tile[r] = make_uint4(hi2[0], hi2[1], lo2[0], lo2[1]);
-  } else {
-    tile[r] = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
-    tile[128 + r] = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
-  }
-}
-
-template <int NG>
-__device__ __forceinline__ void ld_d(uint32_t taddr, uint32_t* d) {
-  if constexpr (NG <= 4) kvlc::tc::tmem_ld8(taddr, d);
-  else kvlc::tc::tmem_ld16(taddr, d);
-}
-template <int NG>
-__device__ __forceinline__ void sum_d(const uint32_t* d, float* out) {  // out[h] = hi + lo columns
-  constexpr int LO = NG <= 4 ? 4 : 8;
-#pragma unroll
-  for (int h = 0; h < NG; ++h) out[h] = __uint_as_float(d[h]) + __uint_as_float(d[LO + h]);
-}
-
-__device__ __forceinline__ float h2f(uint16_t x) { return __half2float(__ushort_as_half(x)); }
-
-// Optional phase tracing (tools/trace_probe.py; build with -DKVLC_TRACE): clock64
-// stamps of token warp 0 / channel warp 4 lane 0 for the first TRACE_CTAS CTAs.
-#ifdef KVLC_TRACE
-constexpr int TRACE_CTAS = 4, TRACE_K = 32, TRACE_PTS = 28;
-__device__ long long g_trace[TRACE_CTAS][TRACE_K + 1][TRACE_PTS];
-#define KVLC_STAMP(k, i)                                                                        \
-  do {                                                                                          \
-    if (blockIdx.x < TRACE_CTAS && (k) < TRACE_K && (threadIdx.x & 127) == 0)                  \
-      g_trace[blockIdx.x][(k) < 0 ? TRACE_K : (k)][i] = clock64();                              \
-  } while (0)
-#define KVLC_STAMP_WARP(k)                                                                      \
-  do {                                                                                          \
-    if (blockIdx.x < TRACE_CTAS && (k) < TRACE_K && (threadIdx.x & 31) == 0)                   \
-      g_trace[blockIdx.x][k][16 + (threadIdx.x >> 5)] = clock64();                              \
-  } while (0)
-#else
-#define KVLC_STAMP_WARP(k) \
-  do {                     \
-  } while (0)
-#define KVLC_STAMP(k, i) \
-  do {                   \
-  } while (0)
-#endif
-
-// Named barriers among the 4 token warps (id 1); id 0 is __syncthreads.
-__device__ __forceinline__ void tbar_sync() { asm volatile("barrier.cta.sync 1, 128;\n" ::: "memory"); }
-__device__ __forceinline__ bool tbar_or(bool pred) {
-  uint32_t r;
-  asm volatile(
-      "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nbarrier.cta.red.or.pred q, 1, 128, p;\nselp.u32 %0, 1, 0, q;\n}\n"
-      : "=r"(r)
-      : "r"((uint32_t)pred)
-      : "memory");
-  return r != 0;
-}
-
-__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// Named barriers: 1 = token warps (128), 2 = loader warps 6-7 (64), 3 = channel warps (128).
-__device__ __forceinline__ void lbar_sync() { asm volatile("barrier.cta.sync 2, 64;\n" ::: "memory"); }
-__device__ __forceinline__ void cbar_sync() { asm volatile("barrier.cta.sync 3, 128;\n" ::: "memory"); }
-
-// The quantized work of a persistent split CTA: one continuous chunk stream
-// over the quantized items it pops from the global queue.  256 threads:
-//   token warps 0-3   (thread = token t of a chunk, TMEM lane t): K-row
-//                     expansion into A_K (double-buffered, so chunk k+1's
-//                     expansion overlaps the QK MMAs of chunk k), the B_QK /
-//                     B_Z rows of chunk k+1 (row = thread index), QK readback,
-//                     online softmax, B_PV row t, per-item totals.
-//   channel warps 4-7 (thread = channel c, TMEM lane c): PV readback into the
-//                     fp32 numerator, V-row expansion into A_V, the item
-//                     records; after the per-chunk barrier
-//                     warp 4 issues the PV MMAs, warp 5 the QK MMAs and warps
-//                     6-7 (the loaders) refill the ring, popping the next items
-//                     from the queue well ahead of use.
-// One CTA barrier per chunk publishes the TMEM / shared operands; QK(k+1)
-// (incl. the key zero term A_ones B_Z) and PV(k) are then issued together and
-// complete on separate mbarriers.  Item boundaries do not drain the pipeline:
-// the per-item state resets in the token / channel roles, and an item's record
-// is published with a release add on its unit's arrival counter.
-// Returns the first non-quantized item popped (or >= nitems).
-template <int NG>
-__device__ int run_quant_stream(const DecArgs& a, int nq, TcSmem& sm, uint32_t tb, uint32_t& qk_ph,
-                                uint32_t& pv_ph) {
+// A quantized split: chunks [lo, hi) of one unit.
+template <int NG, int EXTRA>
+__device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) {
   const kvlc_cache& c = a.c;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool tok = warp < 4, loader = warp >= 6;
-  const int row = tid & 127;
-  const uint32_t lane_addr = tb + ((uint32_t)(32 * (warp & 3)) << 16);
-  const float f4 = __int_as_float((127 - 2 * ((row >> 1) & 3)) << 23);  // 4^-p(row)
-
-  // ---- loaders (warps 6-7): stream chunk L into ring stage L % NSTAGE.  The item
-  // being loaded lives in (uniform) registers; the queue is popped only when it
-  // is exhausted, by one lane, published to the other loader lanes through
-  // shared memory and named barrier 2.
-  auto item_n = [&](int unit, int split) {
-    const int b = unit / c.Hkv;
-    const int n_ch = min(c.n_chunks[b], a.chunk_hi);
-    const int lo = a.chunk_lo + split * a.cpc;
-    return max(0, min(n_ch, lo + a.cpc) - lo);
-  };
-  int ld_j = 0, ld_n = 0, ld_L = 0;
-  bool ld_end = false;
-  size_t ld_cb = 0;
-  uint32_t ticket = loader && tid == 192 ? atomicAdd(a.queue, 1u) : 0u;  // next queue ticket, fetched ahead
-  auto loader_step = [&]() {
-    while (!ld_end && ld_j == ld_n) {
-      if (tid == 192) {
-        const int x = (int)ticket;
-        if (x < nq) ticket = atomicAdd(a.queue, 1u);  // the following one, in flight meanwhile
-        sm.empty_unit = -1;
-        if (x < nq) {
-          const int unit = x / a.nsq, split = x % a.nsq, n = item_n(unit, split);
-          if (n > 0) {
-            sm.items[sm.n_items & (IFIFO - 1)] = QItem{unit, split, n};
-            sm.n_items = sm.n_items + 1;
-          } else {
-            sm.empty_unit = unit;
-            sm.empty_split = split;
-          }
-        } else {
-          sm.next = x;
-          sm.end = ld_L;
-        }
-      }
-      lbar_sync();
-      if (sm.end >= 0) {
-        ld_end = true;
-      } else if (sm.empty_unit >= 0) {  // an item without chunks (short sequence): empty record
-        const int eu = sm.empty_unit;
-        float* rec = a.rec + ((size_t)eu * a.nrec + sm.empty_split) * NG * REC;
-        for (int i = tid - 192; i < NG * REC; i += 64) {
-          const int kk = i % REC;
-          rec[i] = (kk == 0 || kk == 2) ? -INFINITY : 0.f;
-        }
-        lbar_sync();
-        if (tid == 192) red_release_add(a.done + eu, 1u);
-      } else {
-        const int slot = (sm.n_items - 1) & (IFIFO - 1);
-        const QItem q = sm.items[slot];
-        ld_n = q.n;
-        ld_j = 0;
-        ld_cb = (size_t)q.unit * c.max_chunks + a.chunk_lo + (size_t)q.split * a.cpc;
-        // the item's NG query vectors -> sm.qv[slot] (16 B pieces), completes with this chunk's group
-        const int b = q.unit / c.Hkv, kvh = q.unit % c.Hkv;
-        const uint16_t* qsrc = a.q + ((size_t)b * c.Hq + (size_t)kvh * NG) * D;
-        for (int i = tid - 192; i < NG * 16; i += 64)
-          tc::cp_async16(&sm.qv[slot][i >> 4][8 * (i & 15)], qsrc + (i >> 4) * D + 8 * (i & 15));
-      }
-      lbar_sync();  // scratch fields are rewritten by the next pop
-    }
-    if (!ld_end) {
-      ChunkStage& S = sm.stage[ld_L % NSTAGE];
-      const size_t cb = ld_cb + ld_j;
-      const uint4* kc = reinterpret_cast<const uint4*>(c.kcodes + cb * 1024);
-      const uint4* vc = reinterpret_cast<const uint4*>(c.vcodes + cb * 1024);
-      const int i0 = tid - 192;
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) tc::cp_async16(&S.kc[i0 + 64 * jj], kc + i0 + 64 * jj);
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) tc::cp_async16(&S.vc[i0 + 64 * jj], vc + i0 + 64 * jj);
-      {
-        const int which = i0 >> 4, part = i0 & 15;  // 64 pieces: ks, kz, vs, vz
-        const uint16_t* src = (which == 0 ? c.kscale : which == 1 ? c.kzero : which == 2 ? c.vscale : c.vzero) + cb * D;
-        uint16_t* dst = which == 0 ? S.ks : which == 1 ? S.kz : which == 2 ? S.vs : S.vz;
-        tc::cp_async16(dst + 8 * part, src + 8 * part);
-      }
-      ++ld_j;
-      ++ld_L;
-      if (tid == 192) sm.loaded = ld_L;
-    }
-    tc::cp_commit();
-  };
-
-  if (tid == 0) {
-    sm.n_items = 0;
-    sm.loaded = 0;
-    sm.end = -1;
-    sm.next = 0x7fffffff;
-  }
-  for (int i = tid; i < 256; i += QTHREADS) {  // columns beyond the heads stay zero
-    sm.bqk[0][i] = make_uint4(0u, 0u, 0u, 0u);
-    sm.bqk[1][i] = make_uint4(0u, 0u, 0u, 0u);
-    sm.bz[0][i] = make_uint4(0u, 0u, 0u, 0u);
-    sm.bz[1][i] = make_uint4(0u, 0u, 0u, 0u);
-    sm.bpv[0][i] = make_uint4(0u, 0u, 0u, 0u);
-    sm.bpv[1][i] = make_uint4(0u, 0u, 0u, 0u);
-  }
+  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr bool HILO = NG <= 4;
+  // q (fp16, exact from bf16) for this warp's B share: column n = g,
+  // channels 32w + 16e + 2t + {0,1} (+8)
+  uint32_t qs[4];
   {
-    uint32_t ones[8];
+    const int head = HILO ? (g >> 1) : g;
+    const bool valid = head < NG;
+    const uint32_t* qp = reinterpret_cast<const uint32_t*>(
+        a.q + ((size_t)b * c.Hq + (size_t)kvh * NG + (valid ? head : 0)) * D);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) ones[j] = 0x00010001u;  // fp16 2^-24 pairs
-    if (tok) tc::tmem_st8(lane_addr + COL_ONES, ones);
+    for (int i = 0; i < 4; ++i) {
+      const int pair = 16 * warp + 8 * (i >> 1) + t + 4 * (i & 1);
+      const uint32_t raw = valid ? __ldg(qp + pair) : 0u;
+      qs[i] = h2u(__floats2half2_rn(__uint_as_float(raw << 16), __uint_as_float(raw & 0xffff0000u)));
+    }
   }
-  __syncthreads();
-  if (loader) {
-#pragma unroll 1
-    for (int s = 0; s < NSTAGE; ++s) loader_step();
-    tc::cp_wait<NSTAGE - 2>();  // chunks 0, 1
-  }
-  tc::wait_st();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  int L = sm.loaded;
-  if (L == 0) return sm.next;  // no quantized work left
-
-  // token role: q factors (of channel `row`) of the item whose B_QK / B_Z rows are
-  // being built (b_it), and the prefetched raw q of the following item (pre_it)
-  float qf[NG], qz[NG];
-  int b_it = 0;
-  auto q_load = [&](int it, float* dst) {  // staged by the loaders with the item's first chunk
+  WarpState<NG> st;
+  st.init();
+  const int n_ch = min(c.n_chunks[b], a.chunk_hi);
+  const int lo = a.chunk_lo + split * a.cpc;
+  const int hi = min(n_ch, lo + a.cpc);
+  const size_t cb0 = (size_t)unit * c.max_chunks;
+  QuantSmem& q = sm.quant;
+  if (lo < hi) {
+    SliceSrc src;
+    src.init(c, cb0 + lo, warp, lane);
+    const int n = hi - lo;
+    // prologue: stages for chunks 0, 1 (relative) in flight
 #pragma unroll
-    for (int h = 0; h < NG; ++h) dst[h] = bf2f(sm.qv[it & (IFIFO - 1)][h][row]);
-  };
-  auto q_set = [&](const float* qv) {
-#pragma unroll
-    for (int h = 0; h < NG; ++h) {
-      qf[h] = qv[h] * (C0 * QK_SCALE) * f4;
-      qz[h] = qv[h] * (C0 * QK_SCALE);
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < n) src.issue(q.stage[s][warp], lane, s);
+      cp_commit();
     }
-  };
-  auto build_bqk = [&](int k) {  // token role: B_QK / B_Z row `row` of stream chunk k
-    const ChunkStage& S = sm.stage[k % NSTAGE];
-    const float s = h2f(S.ks[row]), z = h2f(S.kz[row]);
-    float x[NG], y[NG];
-#pragma unroll
-    for (int h = 0; h < NG; ++h) {
-      x[h] = qf[h] * s;
-      y[h] = qz[h] * z;
-    }
-    write_brow<NG>(sm.bqk[k & 1], row, x);
-    write_brow<NG>(sm.bz[k & 1], row, y);
-  };
-  auto issue_qk = [&](int k) {  // warp 5
-    tc::mma16_qk_commit_w(tb + COL_DQK, tb + COL_AK + 64u * (uint32_t)(k & 1), tc::bdesc(tc::smem_u32(sm.bqk[k & 1])),
-                          tb + COL_ONES, tc::bdesc(tc::smem_u32(sm.bz[k & 1])), &sm.mqk);
-  };
-  auto issue_pv = [&](int k) {  // warp 4
-    tc::mma8_commit_w(tb + COL_DPV, tb + COL_AV, tc::bdesc(tc::smem_u32(sm.bpv[k & 1])), &sm.mpv);
-  };
-
-  // prologue: operands of chunk 0, QK(0)
-  if (tok) {
-    float q0[NG];
-    q_load(0, q0);
-    q_set(q0);
-    expand_row(sm.stage[0].kc, row, lane_addr + COL_AK);
-    build_bqk(0);
-  } else {
-    expand_row(sm.stage[0].vc, row, lane_addr + COL_AV);
-  }
-  tc::wait_st();
-  tc::fence_proxy_async();
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 5) {
-    tc::fence_after_sync();
-    issue_qk(0);
-  }
-
-  // token role: reference point o (log2 units), l, sum p z_v, true max; channel role: numerator acc in frame oc
-  float o[NG], l[NG], zs[NG], mt[NG], acc[NG], oc[NG];
-  auto reset_tok = [&]() {
-#pragma unroll
-    for (int h = 0; h < NG; ++h) {
-      o[h] = -INFINITY;
-      l[h] = 0.f;
-      zs[h] = 0.f;
-      mt[h] = -INFINITY;
-    }
-  };
-  auto reset_chn = [&]() {
-#pragma unroll
-    for (int h = 0; h < NG; ++h) {
-      acc[h] = 0.f;
-      oc[h] = -INFINITY;
-    }
-  };
-  reset_tok();
-  reset_chn();
-  // channel role: PV of stream chunk k (frame ob[k & 1]) -> acc; if k ends its item, publish the record
-  int pend_unit = -1, pend_k = 0;  // tid 224: an item record written at chunk pend_k, not yet released
-  auto drain_pv = [&](int k, int it, bool last) {
-    uint32_t dp[16];
-    ld_d<NG>(lane_addr + COL_DPV, dp);
-    tc::wait_ld();
-    float d[NG];
-    sum_d<NG>(dp, d);
-#pragma unroll
-    for (int h = 0; h < NG; ++h) {
-      const float on = sm.ob[k & 1][h];
-      if (on != oc[h]) {  // warp-uniform; rare after an item's first chunk
-        acc[h] *= oc[h] == -INFINITY ? 0.f : exp2f(oc[h] - on);
-        oc[h] = on;
-      }
-      acc[h] = fmaf(d[h], 16777216.f, acc[h]);
-    }
-    if (last) {
-      const QItem q = sm.items[it & (IFIFO - 1)];
-      float* rec = a.rec + ((size_t)q.unit * a.nrec + q.split) * NG * REC;
-      const float(*tr)[8][4] = sm.itred[it & 1];
-#pragma unroll
-      for (int h = 0; h < NG; ++h) {
-        const float Lh = (tr[0][h][0] + tr[1][h][0]) + (tr[2][h][0] + tr[3][h][0]);
-        const float Z = (tr[0][h][1] + tr[1][h][1]) + (tr[2][h][1] + tr[3][h][1]);
-        const float MT = fmaxf(fmaxf(tr[0][h][2], tr[1][h][2]), fmaxf(tr[2][h][2], tr[3][h][2]));
-        float* r = rec + h * REC;
-        if (row == 0) *reinterpret_cast<float4*>(r) = make_float4(oc[h], Lh, MT, 0.f);
-        r[4 + row] = acc[h] + Z;  // numerator of channel row: sum_t p_t (s_t code_t + z_t), rotated basis
-      }
-      if (tid == 224) {  // released a few chunks later, when its writes are long complete (no fence stall)
-        if (pend_unit >= 0) red_release_add(a.done + pend_unit, 1u);  // short items: release the older one now
-        pend_unit = q.unit;
-        pend_k = k;
-      }
-      reset_chn();
-    }
-  };
-
-  int ci = 0, cj = 0;  // item (FIFO index) and chunk within it of stream chunk k
-  int k = 0;
-  for (; k < L; ++k) {
-    const int n_ci = sm.items[ci & (IFIFO - 1)].n;
-    const bool first = cj == 0, last = cj == n_ci - 1;
-    const bool more = k + 1 < L;
-    if (tok) {
-      KVLC_STAMP(k, 0);
-      // chunk k+1's K rows into the other A_K buffer, its B_QK / B_Z rows into the
-      // other B buffers (their last reader QK(k-1) is complete)
-      if (more) {
-        expand_row(sm.stage[(k + 1) % NSTAGE].kc, row, lane_addr + COL_AK + 64u * (uint32_t)((k + 1) & 1));
-        const int nb = last ? ci + 1 : ci;  // item of chunk k+1
-        if (nb != b_it) {                   // a new item: its q (staged in shared memory)
-          float qn[NG];
-          q_load(nb, qn);
-          q_set(qn);
-          b_it = nb;
-        }
-        build_bqk(k + 1);
-      }
-      KVLC_STAMP(k, 1);
-      tc::mbar_wait(&sm.mqk, (qk_ph + (uint32_t)k) & 1u);  // QK(k) complete
-      tc::fence_after_sync();
-      KVLC_STAMP(k, 2);
-      float l2[NG];
-      {
-        uint32_t dq[16];
-        ld_d<NG>(lane_addr + COL_DQK, dq);
-        tc::wait_ld();
-        sum_d<NG>(dq, l2);
-      }
-      if (first) reset_tok();
-      bool ev = false;
-#pragma unroll
-      for (int h = 0; h < NG; ++h) {
-        l2[h] *= 16777216.f / QK_SCALE;  // logit incl. the key zero term, log2 units (C0 folded into q)
-        ev |= l2[h] > o[h] + LAZY;
-      }
-      if (tbar_or(ev)) {  // move the reference point (item start, or a new maximum)
-#pragma unroll
-        for (int h = 0; h < NG; ++h) {
-          const float m = warp_max(l2[h]);
-          if (lane == 0) sm.red[warp][h][0] = m;
-        }
-        tbar_sync();
-#pragma unroll
-        for (int h = 0; h < NG; ++h) {
-          const float m = fmaxf(fmaxf(sm.red[0][h][0], sm.red[1][h][0]), fmaxf(sm.red[2][h][0], sm.red[3][h][0]));
-          const float on = fmaxf(o[h], m);
-          const float f = o[h] == -INFINITY ? 0.f : exp2f(o[h] - on);
-          l[h] *= f;
-          zs[h] *= f;
-          o[h] = on;
-        }
-        tbar_sync();  // red[] is reused
-      }
-      KVLC_STAMP(k, 3);
-      const ChunkStage& S = sm.stage[k % NSTAGE];
-      const float sv = h2f(S.vs[row]) * f4, zv = h2f(S.vz[row]);
-      float pv[NG];
-#pragma unroll
-      for (int h = 0; h < NG; ++h) {
-        const float p = fast_exp2(l2[h] - o[h]);
-        l[h] += p;
-        zs[h] = fmaf(p, zv, zs[h]);
-        mt[h] = fmaxf(mt[h], l2[h]);
-        pv[h] = p * sv;
-      }
-      write_brow<NG>(sm.bpv[k & 1], row, pv);
-      if (row < NG) sm.ob[k & 1][row] = o[row];
-      if (last) {  // per-warp item totals for the channel role's record
-#pragma unroll
-        for (int h = 0; h < NG; ++h) {
-          const float ls = warp_sum(l[h]), zz = warp_sum(zs[h]), mm = warp_max(mt[h]);
-          if (lane == 0) {
-            sm.itred[ci & 1][warp][h][0] = ls;
-            sm.itred[ci & 1][warp][h][1] = zz;
-            sm.itred[ci & 1][warp][h][2] = mm;
-          }
-        }
-      }
-      KVLC_STAMP(k, 4);
-    } else {
-      KVLC_STAMP(k, 8);
-      if (tid == 224 && pend_unit >= 0 && k >= pend_k + 3) {  // its writes are long complete: cheap fence
-        red_release_add(a.done + pend_unit, 1u);
-        pend_unit = -1;
-      }
-      if (k > 0) {
-        tc::mbar_wait(&sm.mpv, (pv_ph + (uint32_t)(k - 1)) & 1u);  // PV(k-1) complete: D_PV and A_V are free
-        tc::fence_after_sync();
-        KVLC_STAMP(k, 9);
-        // stream chunk k-1 ended its item iff chunk k starts one
-        drain_pv(k - 1, first ? ci - 1 : ci, first);
-        KVLC_STAMP(k, 10);
-        expand_row(sm.stage[k % NSTAGE].vc, row, lane_addr + COL_AV);
-      }
-      KVLC_STAMP(k, 11);
-    }
-    if (loader) tc::cp_wait<NSTAGE - 3>();  // chunk k+2 landed; visible to all after the barrier
-    tc::wait_st();
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    KVLC_STAMP_WARP(k);
+    cp_wait<STAGES - 2>();
+    __syncwarp();
+    build_b<NG>(q, 0, q.stage[0][warp], qs, warp, lane);
     __syncthreads();
-    KVLC_STAMP(k, tok ? 5 : 13);
-    if (warp == 5) {
-      tc::fence_after_sync();
-      if (more) issue_qk(k + 1);
-    } else if (warp == 4) {
-      tc::fence_after_sync();
-      issue_pv(k);
-    } else if (loader) {
-      loader_step();  // chunk k's stage is fully consumed
+    int s_cur = 0;
+    for (int k = 0; k < n; ++k) {
+      const int buf = k & 1;
+      const int s_next = s_cur == STAGES - 1 ? 0 : s_cur + 1;
+      const int s_fill = s_cur == 0 ? STAGES - 1 : s_cur - 1;   // freed by chunk k-1
+      if (k + STAGES - 1 < n) src.issue(q.stage[s_fill][warp], lane, k + STAGES - 1);
+      cp_commit();
+      quant_chunk<NG, EXTRA>(q.stage[s_cur][warp], q, buf, st, lane);
+      if (k + 1 < n) {
+        cp_wait<STAGES - 2>();   // chunk k+1 has landed (only k+2 may be pending)
+        __syncwarp();
+        build_b<NG>(q, buf ^ 1, q.stage[s_next][warp], qs, warp, lane);
+      }
+      __syncthreads();
+      s_cur = s_next;
     }
-    KVLC_STAMP(k, tok ? 6 : 14);
-    if (last) {
-      ++ci;
-      cj = 0;
-    } else {
-      ++cj;
-    }
-    // sm.loaded may be bumped concurrently by the loaders of this iteration; either
-    // value gives the same answer to "chunk k+2 exists" (the ring runs NSTAGE >= 3 ahead,
-    // and a finished stream no longer changes it)
-    L = sm.loaded;
+    cp_wait<0>();
   }
-  if (!tok) {  // last PV and record
-    tc::mbar_wait(&sm.mpv, (pv_ph + (uint32_t)(k - 1)) & 1u);
-    tc::fence_after_sync();
-    drain_pv(k - 1, ci - 1, true);
-    cbar_sync();  // every channel thread has written the last record
-    if (tid == 224) red_release_add(a.done + pend_unit, 1u);
-  }
-  if (loader) tc::cp_wait<0>();
-  tc::fence_before_sync();
+  __syncthreads();   // the record area aliases the pipeline buffers
+  warp_store<NG, true>(st, sm.rec + warp * NG * REC, lane);
   __syncthreads();
-  qk_ph += (uint32_t)k;
-  pv_ph += (uint32_t)k;
-  return sm.next;
+  cta_merge<NG>(sm.rec, a.rec + ((size_t)unit * a.nrec + split) * NG * REC);
 }
