@@ -14,7 +14,9 @@
 // float16(fp64 value).  k_err / v_q for the state update use the float64
 // scales, as cache.py:153-154 does.
 #include "kvlc_common.cuh"
+#include "kvlc_tc.cuh"
 
+#include <algorithm>
 #include <cstring>
 
 namespace kvlc {
@@ -448,6 +450,436 @@ __global__ void export_chunk_kernel(kvlc_cache c, int unit, int chunk, uint32_t*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Prefill flush with the adapter-state update on the 5th-generation tensor
+// cores (tcgen05).  One CTA per (unit, feature half h, chunk range): W_h (the
+// 128 features of W1k or W2k, fp16 hi + lo) stays resident in shared memory;
+// per chunk (flush_group, cache.py:132-158):
+//   K1  keys, channel-wise codes (fp64 decisions, bit-exact) and k_err = k - k_hat
+//       -> A_phi = k_err [128 tokens x 128 channels] (fp16 hi / lo tiles);
+//   K2  values: fp64 FWHT, token-wise codes, v_q -> B_S = [v_q | 1 | 0] [128 tokens x 144];
+//   phi Z = k_err W_h (3 MMAs passes hi*hi + hi*lo + lo*hi, M = 128 tokens, N = 128,
+//       f32 in TMEM), row softmax (feature_map, adapter.py:80-88) -> A_S = Phi^T;
+//   S   D_S += Phi^T [v_q | 1] (M = 128 features, N = 144, accumulated in TMEM over the
+//       CTA's chunks): D_S[f][c] = S[c][h*128 + f], D_S[f][128] = P[h*128 + f].
+// Codes / metadata are written by the half-0 CTA.  Operand tiles are MN-major
+// without swizzle (core matrix 8 x 16 B, LBO 128 B between K groups, SBO 2048 B
+// between M/N groups), see kvlc_tc.cuh.
+constexpr int FT_THREADS = 256;
+constexpr int FT_TILE = 32768;              // [128][128] fp16 tile
+constexpr int FT_NS = 144;                  // B_S columns: v_q (128), ones (1), zero padding
+constexpr int FT_TILE_S = FT_NS / 8 * 2048;  // [128][144] fp16 tile
+constexpr uint32_t FT_COL_PHI = 0, FT_COL_S = 128, FT_TMEM = 512;
+constexpr uint32_t FT_IDESC_PHI = (1u << 4) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | (8u << 24);
+constexpr uint32_t FT_IDESC_S = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(FT_NS >> 3) << 17) | (8u << 24);
+
+struct FtSmem {
+  uint8_t w[2][FT_TILE];     // W_h hi / lo: B of the phi GEMM, [K = channel][N = feature]
+  uint8_t a[2][FT_TILE];     // A_phi (k_err, [M = token][K = channel]) then A_S (Phi^T, [M = feature][K = token])
+  uint8_t bs[2][FT_TILE_S];  // B_S hi / lo: [K = token][N = 144]
+  uint8_t codes[G * D];      // value codes [token][channel] (for the packed V words)
+  double2 kpar[D];           // per channel (min, scale) of the key chunk
+  float red[2][FT_THREADS];
+  uint64_t mphi, ms;
+  uint32_t tbase;
+};
+
+__device__ __forceinline__ int ft_off(int mn, int k) {  // byte offset of element (mn, k) in an MN-major tile
+  return (mn & 7) * 2 + (k & 7) * 16 + (mn >> 3) * 2048 + (k >> 3) * 128;
+}
+__device__ __forceinline__ void ft_hilo(float x, __half& hi, __half& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(x - __half2float(hi));
+}
+__device__ __forceinline__ uint64_t ft_desc(const void* p) { return tc::bdesc(tc::smem_u32(p)); }
+
+// 3 passes (hi*hi, hi*lo, lo*hi) of a K = 128 contraction: 24 MMAs, one elected lane.
+__device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE], const uint8_t* b0, const uint8_t* b1,
+                                        uint32_t idesc, bool accumulate) {
+  const uint64_t ah = ft_desc(a[0]), al = ft_desc(a[1]), bh = ft_desc(b0), bl = ft_desc(b1);
+  const uint64_t pa[3] = {ah, ah, al}, pb[3] = {bh, bl, bh};
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t acc = (accumulate || p > 0 || j > 0) ? 1u : 0u;
+      asm volatile(
+          "{\n.reg .pred q, e;\nsetp.ne.b32 q, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+          "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(d),
+          "l"(pa[p] + 16 * j), "l"(pb[p] + 16 * j), "r"(idesc), "r"(acc)
+          : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs a, const SeqInfo seq,
+                                                                 const uint8_t* __restrict__ wtiles) {
+  extern __shared__ __align__(1024) uint8_t ft_raw[];
+  FtSmem& sm = *reinterpret_cast<FtSmem*>(ft_raw);
+  const kvlc_cache& c = a.c;
+  const int unit = blockIdx.y, split = blockIdx.x, h = blockIdx.z;
+  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nf = seq.nflush[b];
+  const int c_lo = split * a.cpc, c_hi = min(nf, c_lo + a.cpc);
+  if (c_lo >= c_hi) return;
+  const bool writer = h == 0;  // the half-0 CTA stores codes and metadata
+
+  // resident W_h tiles (prepared by prep_wtiles_kernel), constant B_S columns, TMEM, barriers
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + h) * 2 * FT_TILE);
+    uint4* dst = reinterpret_cast<uint4*>(sm.w[0]);
+    for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
+    tc::cp_commit();
+  }
+  for (int i = tid; i < 2 * G * 2; i += FT_THREADS) {  // tile x token x column group 16 / 17
+    const int tile = i / (2 * G), t = (i >> 1) % G, grp = 16 + (i & 1);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (tile == 0 && grp == 16) v.x = 0x3C00u;  // hi tile, column 128 = 1.0 (P); lo and padding 0
+    *reinterpret_cast<uint4*>(sm.bs[tile] + grp * 2048 + (t >> 3) * 128 + (t & 7) * 16) = v;
+  }
+  if (warp == 0) tc::tmem_alloc(&sm.tbase, FT_TMEM);
+  if (tid == 0) {
+    tc::mbar_init(&sm.mphi, 1);
+    tc::mbar_init(&sm.ms, 1);
+    tc::mbar_fence_init();
+  }
+  tc::cp_wait<0>();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tb = sm.tbase;
+  const uint32_t lane_addr = tb + ((uint32_t)(32 * (warp & 3)) << 16);
+
+  for (int ci = c_lo; ci < c_hi; ++ci) {
+    const int it = ci - c_lo;
+    const int64_t tok0 = (int64_t)ci * G;
+    const uint16_t* K = a.ksrc + unit * a.k_unit + tok0 * a.k_t;
+    const uint16_t* V = a.vsrc + unit * a.v_unit + tok0 * a.v_t;
+    const size_t cb = (size_t)unit * c.max_chunks + ci;
+    if (it > 0) {  // the previous S GEMM has read A_S (aliased by A_phi) and B_S
+      tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);
+      tc::fence_after_sync();
+    }
+
+    // ---- K1: keys, channel-wise.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3
+    // (16-B vector loads).  Codes in fp32 with the exact fp64 decision near rounding
+    // ties (quantize.py:202-207 bit-exact); the lane also packs the fragment-native
+    // K words of its 4 tokens x 16 channels (pack_k_word layout).
+    {
+      const int ch0 = 16 * warp;
+      float x[4][16];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint4* src = reinterpret_cast<const uint4*>(K + (size_t)(4 * lane + r) * D + ch0);
+        const uint4 p0 = __ldg(src), p1 = __ldg(src + 1);
+        const uint32_t wv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          x[r][2 * e] = __uint_as_float(wv[e] << 16);
+          x[r][2 * e + 1] = __uint_as_float(wv[e] & 0xffff0000u);
+        }
+      }
+      // channel min / max over the 128 tokens: reduce-scatter over the lanes
+      float mn16[16], mx16[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        mn16[e] = fminf(fminf(x[0][e], x[1][e]), fminf(x[2][e], x[3][e]));
+        mx16[e] = fmaxf(fmaxf(x[0][e], x[1][e]), fmaxf(x[2][e], x[3][e]));
+      }
+      int n = 16;
+#pragma unroll
+      for (int sft = 16; sft >= 2; sft >>= 1) {
+        const bool up = lane & sft;
+        n >>= 1;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (e < n) {
+            const float sa = up ? mn16[e] : mn16[e + n], ka = up ? mn16[e + n] : mn16[e];
+            const float sb = up ? mx16[e] : mx16[e + n], kb = up ? mx16[e + n] : mx16[e];
+            mn16[e] = fminf(ka, __shfl_xor_sync(0xffffffffu, sa, sft));
+            mx16[e] = fmaxf(kb, __shfl_xor_sync(0xffffffffu, sb, sft));
+          }
+        }
+      }
+      mn16[0] = fminf(mn16[0], __shfl_xor_sync(0xffffffffu, mn16[0], 1));
+      mx16[0] = fmaxf(mx16[0], __shfl_xor_sync(0xffffffffu, mx16[0], 1));
+      // lane pair (2e', 2e'+1) owns channel ch0 + e(l): bits of l >> 1 select the kept halves
+      const int own = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+      if ((lane & 1) == 0) {
+        const double mn = (double)mn16[0], mx = (double)mx16[0];
+        const double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
+        sm.kpar[ch0 + own] = make_double2(mn, scale);
+        if (writer) {
+          c.kscale[cb * D + ch0 + own] = __half_as_ushort(__double2half(scale));
+          c.kzero[cb * D + ch0 + own] = __half_as_ushort(__double2half(mn));
+        }
+      }
+      __syncwarp();
+      uint32_t cw[4] = {0u, 0u, 0u, 0u};  // K words t0 = 0..3 of this lane's tokens
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const double2 pr = sm.kpar[ch0 + e];
+        const double mn = pr.x, scale = pr.y;
+        const float mnf = (float)mn, scf = (float)scale, invf = scale > 0.0 ? (float)(1.0 / scale) : 0.f;
+        __half hi[4], lo[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          uint32_t code = 0u;
+          if (scale > 0.0) {
+            const float q = (x[r][e] - mnf) * invf;
+            const float fr = q - floorf(q);
+            if (fabsf(fr - 0.5f) < 1e-5f) code = code_of((double)x[r][e], mn, scale, 3);  // near a tie: exact
+            else code = (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f);
+          }
+          ft_hilo(x[r][e] - fmaf((float)code, scf, mnf), hi[r], lo[r]);
+          // byte q of word t0 holds channel 16kt + 2t0 + {0,8,1,9}[q]; bit pair r holds token 4l + r
+          const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
+          cw[t0] |= code << (8 * qb + 2 * r);
+        }
+        // A_phi element (token 4l + r, channel ch0 + e): 4 consecutive tokens are 8 contiguous bytes
+        *reinterpret_cast<uint2*>(sm.a[0] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(hi);
+        *reinterpret_cast<uint2*>(sm.a[1] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(lo);
+      }
+      if (writer) {
+        const int wt = lane >> 3, g = lane & 7;  // tokens 32 wt + 4 g + r
+#pragma unroll
+        for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = cw[t0];
+      }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {  // phi GEMM: Z = k_err W_h
+      tc::fence_after_sync();
+      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false);
+      tc::mma_commit_w(&sm.mphi);
+    }
+
+    // ---- K2: values, FWHT post-rotation (fp32, guarded), token-wise quantization ----
+    // The fp32 FWHT differs from the reference's fp64 dense x @ H in the last bits:
+    // a token whose quotient lies near a rounding tie or whose scale / zero lies near
+    // an fp16 rounding midpoint is re-evaluated in the reference's exact order.
+    for (int t = warp; t < G; t += FT_THREADS / 32) {
+      float xf[4];
+      {
+        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(V + (size_t)t * a.v_t + lane * 4));
+        xf[0] = __uint_as_float(raw.x << 16);
+        xf[1] = __uint_as_float(raw.x & 0xffff0000u);
+        xf[2] = __uint_as_float(raw.y << 16);
+        xf[3] = __uint_as_float(raw.y & 0xffff0000u);
+      }
+      float u0 = xf[0] + xf[1], u1 = xf[0] - xf[1], u2 = xf[2] + xf[3], u3 = xf[2] - xf[3];
+      xf[0] = u0 + u2;
+      xf[2] = u0 - u2;
+      xf[1] = u1 + u3;
+      xf[3] = u1 - u3;
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float o = __shfl_xor_sync(0xffffffffu, xf[e], k);
+          xf[e] = (lane & k) ? (o - xf[e]) : (xf[e] + o);
+        }
+      }
+      const float hsf = 0.08838834764831845f;
+      float mnf = INFINITY, mxf = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        xf[e] *= hsf;
+        mnf = fminf(mnf, xf[e]);
+        mxf = fmaxf(mxf, xf[e]);
+      }
+      mnf = warp_min(mnf);
+      mxf = warp_max(mxf);
+      double x[4], mn = (double)mnf, mx = (double)mxf;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = (double)xf[e];
+      double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
+      double inv = scale > 0.0 ? 1.0 / scale : 0.0;
+      // fp32 FWHT error bound (7 add stages, the scaled result): a few ulps of the token's
+      // largest magnitude; the guards below are widened accordingly
+      const double big = fmax(fabs(mn), fabs(mx)), ferr = 4e-6 * big;
+      auto near_mid = [](double v, double rel) {  // fp16 rounding could differ from the fp64 reference value
+        return __half_as_ushort(__double2half(v * (1.0 - rel))) != __half_as_ushort(__double2half(v * (1.0 + rel)));
+      };
+      bool amb = near_mid(mn, ferr / fmax(fabs(mn), 1e-30) + 1e-9) ||
+                 (scale > 0.0 && near_mid(scale, 2.0 * ferr / (mx - mn) + 1e-9));
+      const double qtol = 1e-5 + 4.0 * ferr * inv;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double r = __dsub_rn(x[e], mn) * inv;
+        amb |= scale > 0.0 && fabs(r - floor(r) - 0.5) < qtol;
+      }
+      const double hs = 1.0 / sqrt((double)D);
+      if (__any_sync(0xffffffffu, amb)) {
+        // fp64 FWHT: agrees with the dense fp64 x @ H to an ulp
+        double y[4];
+        {
+          const uint2 raw = __ldg(reinterpret_cast<const uint2*>(V + (size_t)t * a.v_t + lane * 4));
+          y[0] = (double)__uint_as_float(raw.x << 16);
+          y[1] = (double)__uint_as_float(raw.x & 0xffff0000u);
+          y[2] = (double)__uint_as_float(raw.y << 16);
+          y[3] = (double)__uint_as_float(raw.y & 0xffff0000u);
+        }
+        double w0 = y[0] + y[1], w1 = y[0] - y[1], w2 = y[2] + y[3], w3 = y[2] - y[3];
+        y[0] = w0 + w2;
+        y[2] = w0 - w2;
+        y[1] = w1 + w3;
+        y[3] = w1 - w3;
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const double o = __shfl_xor_sync(0xffffffffu, y[e], k);
+            y[e] = (lane & k) ? (o - y[e]) : (y[e] + o);
+          }
+        }
+        mn = INFINITY;
+        mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          x[e] = y[e] * hs;
+          mn = fmin(mn, x[e]);
+          mx = fmax(mx, x[e]);
+        }
+        mn = warp_min_d(mn);
+        mx = warp_max_d(mx);
+        scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
+        inv = scale > 0.0 ? 1.0 / scale : 0.0;
+        bool amb2 = near_half_tie(scale) || near_half_tie(mn);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double r = __dsub_rn(x[e], mn) * inv;
+          amb2 |= scale > 0.0 && fabs(r - floor(r) - 0.5) < 1e-9;
+        }
+        if (__any_sync(0xffffffffu, amb2)) {  // a genuine tie: the reference's dense x @ H order
+          mn = INFINITY;
+          mx = -INFINITY;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int ch = lane * 4 + e;
+            double acc = 0.0;
+            for (int j = 0; j < D; ++j) {
+              const double hj = (__popc((unsigned)(j & ch)) & 1) ? -hs : hs;
+              acc = fma((double)bf2f(V[t * a.v_t + j * a.v_c]), hj, acc);
+            }
+            x[e] = acc;
+            mn = fmin(mn, acc);
+            mx = fmax(mx, acc);
+          }
+          mn = warp_min_d(mn);
+          mx = warp_max_d(mx);
+          scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
+          inv = scale > 0.0 ? 1.0 / scale : 0.0;
+        }
+      }
+      __half hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t code = code2(x[e], mn, scale, inv);
+        sm.codes[t * D + lane * 4 + e] = (uint8_t)code;
+        ft_hilo((float)__dadd_rn(__dmul_rn((double)code, scale), mn), hi[e], lo[e]);
+      }
+      // B_S element (token t, channel 4 lane + e): 4 consecutive channels are 8 contiguous bytes
+      *reinterpret_cast<uint2*>(sm.bs[0] + ft_off(lane * 4, t)) = *reinterpret_cast<uint2*>(hi);
+      *reinterpret_cast<uint2*>(sm.bs[1] + ft_off(lane * 4, t)) = *reinterpret_cast<uint2*>(lo);
+      if (writer && lane == 0) {
+        c.vscale[cb * G + t] = __half_as_ushort(__double2half(scale));
+        c.vzero[cb * G + t] = __half_as_ushort(__double2half(mn));
+      }
+    }
+    __syncthreads();
+    if (writer)
+      for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word(sm.codes, wi);
+
+    // ---- softmax of Z (token rows): warps w and w + 4 share TMEM lanes 32 (w & 3) .., 64 columns each ----
+    tc::mbar_wait(&sm.mphi, (uint32_t)it & 1u);
+    tc::fence_after_sync();
+    {
+      const int t = 32 * (warp & 3) + lane, part = warp >> 2;
+      float z[64];
+      tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part, reinterpret_cast<uint32_t*>(z));
+      tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part + 32, reinterpret_cast<uint32_t*>(z) + 32);
+      tc::wait_ld();
+      float m = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) m = fmaxf(m, z[i]);
+      sm.red[part][t] = m;
+      __syncthreads();
+      m = fmaxf(sm.red[0][t], sm.red[1][t]);
+      float ssum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        z[i] = expf(z[i] - m);
+        ssum += z[i];
+      }
+      __syncthreads();
+      sm.red[part][t] = ssum;
+      __syncthreads();
+      const float inv = 1.f / (sm.red[0][t] + sm.red[1][t]);
+      // A_S = Phi^T: element (feature f, token t); 8 consecutive features are 16 contiguous bytes
+#pragma unroll
+      for (int f8 = 0; f8 < 64; f8 += 8) {
+        __half hi[8], lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ft_hilo(z[f8 + e] * inv, hi[e], lo[e]);
+        *reinterpret_cast<uint4*>(sm.a[0] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(hi);
+        *reinterpret_cast<uint4*>(sm.a[1] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(lo);
+      }
+    }
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {  // S GEMM: D_S += Phi^T [v_q | 1]
+      tc::fence_after_sync();
+      ft_gemm(tb + FT_COL_S, sm.a, sm.bs[0], sm.bs[1], FT_IDESC_S, it > 0);
+      tc::mma_commit_w(&sm.ms);
+    }
+  }
+
+  // ---- drain D_S: row f (TMEM lane), columns c (S[c][h*128 + f]) and 128 (P) ----
+  tc::mbar_wait(&sm.ms, (uint32_t)(c_hi - c_lo - 1) & 1u);
+  tc::fence_after_sync();
+  {
+    const int f = 32 * (warp & 3) + lane, part = warp >> 2;
+    float* S = a.s_out ? a.s_out + ((size_t)unit * a.splits + split) * D * RANK : c.S + (size_t)unit * D * RANK;
+    float* P = a.p_out ? a.p_out + ((size_t)unit * a.splits + split) * RANK : c.P + (size_t)unit * RANK;
+    float d[32];
+#pragma unroll 1
+    for (int c0 = 64 * part; c0 < 64 * part + 64; c0 += 32) {
+      tc::tmem_ld32(lane_addr + FT_COL_S + c0, reinterpret_cast<uint32_t*>(d));
+      tc::wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) S[(size_t)(c0 + i) * RANK + h * HALF + f] += d[i];
+    }
+    if (part == 0) {
+      uint32_t pv[8];
+      tc::tmem_ld8(lane_addr + FT_COL_S + D, pv);
+      tc::wait_ld();
+      P[h * HALF + f] += __uint_as_float(pv[0]);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tb, FT_TMEM);
+}
+
+// W1k / W2k (fp32 [Hkv][128][128]) -> fp16 hi / lo B tiles of the phi GEMM,
+// [kvh][half][hi, lo][FT_TILE]: element (k = channel, n = feature).
+__global__ void prep_wtiles_kernel(kvlc_adapter ad, int Hkv, uint8_t* __restrict__ out) {
+  const int kvh = blockIdx.y, h = blockIdx.z;
+  const float* W = (h == 0 ? ad.w1k : ad.w2k) + (size_t)kvh * D * HALF;
+  uint8_t* hi = out + ((size_t)kvh * 2 + h) * 2 * FT_TILE;
+  uint8_t* lo = hi + FT_TILE;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D * HALF; i += gridDim.x * blockDim.x) {
+    const int ch = i / HALF, f = i % HALF;
+    __half x, y;
+    ft_hilo(W[i], x, y);
+    *reinterpret_cast<__half*>(hi + ft_off(f, ch)) = x;
+    *reinterpret_cast<__half*>(lo + ft_off(f, ch)) = y;
+  }
+}
+
 int check_cache(const kvlc_cache* c) {
   KVLC_REQUIRE(c != nullptr, "null cache descriptor");
   KVLC_REQUIRE(c->B >= 1 && c->Hkv >= 1 && c->Hq >= c->Hkv && c->Hq % c->Hkv == 0 &&
@@ -477,7 +909,9 @@ size_t kvlc_prefill_workspace(const kvlc_cache* c, int64_t n_tok) {
   int units = c->B * c->Hkv;
   int splits = (int)((nf + 3) / 4);
   if (splits < 1) splits = 1;
-  return align_up((size_t)units * splits * (D * RANK + RANK) * sizeof(float));
+  // S / P partials (the tensor-core path uses fewer splits) + the W hi / lo tiles
+  return align_up((size_t)units * splits * (D * RANK + RANK) * sizeof(float)) +
+         align_up((size_t)c->Hkv * 2 * 2 * FT_TILE);
 }
 
 int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k, const uint16_t* v,
@@ -502,23 +936,53 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     seq.len[b] = lens_host[b];
     if (nf > max_nf) max_nf = nf;
   }
-  // cpc chunks per CTA: enough CTAs to cover the SMs, few enough partials
-  const int cpc = 4;
-  const int splits = max_nf > 0 ? (max_nf + cpc - 1) / cpc : 1;
   const bool use_ad = adapter_on(ad);
-  if (max_nf > 0) {
-    float *s_part = nullptr, *p_part = nullptr;
-    if (use_ad) {
-      Arena ar(ws, ws_bytes);
-      s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
-      KVLC_REQUIRE(s_part, "prefill workspace too small (%zu bytes)", ws_bytes);
-      p_part = s_part + (size_t)units * splits * D * RANK;
-      KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
-    }
+  if (max_nf > 0 && use_ad) {
+    // tensor-core path: one CTA per (unit, feature half, chunk range), <= one wave
+    static int sms = [] {
+      int dev = 0, n = 148;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return n;
+    }();
+    const int ws_splits = (int)std::max<int64_t>(1, (n_tok / KVLC_G + 3) / 4);  // kvlc_prefill_workspace bound
+    const int splits = std::max(1, std::min(std::min(max_nf, ws_splits), sms / (2 * units)));
+    const int cpc = (max_nf + splits - 1) / splits;
+    Arena ar(ws, ws_bytes);
+    float* s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
+    uint8_t* wtiles = ar.take<uint8_t>((size_t)c->Hkv * 2 * 2 * FT_TILE);
+    KVLC_REQUIRE(s_part && wtiles, "prefill workspace too small (%zu bytes)", ws_bytes);
+    float* p_part = s_part + (size_t)units * splits * D * RANK;
+    KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
+    prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
+    if ((rc = check_launch("prep_wtiles"))) return rc;
     FlushArgs a{};
     a.c = *c;
-    if (use_ad) a.ad = *ad;
-    a.use_adapter = use_ad ? 1 : 0;
+    a.ad = *ad;
+    a.use_adapter = 1;
+    a.ksrc = k;
+    a.vsrc = v;
+    a.k_unit = n_tok * D;
+    a.k_t = D;
+    a.k_c = 1;
+    a.v_unit = n_tok * D;
+    a.v_t = D;
+    a.v_c = 1;
+    a.cpc = cpc;
+    a.s_out = s_part;
+    a.p_out = p_part;
+    a.splits = splits;
+    KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
+    flush_tc_kernel<<<dim3(splits, units, 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
+    if ((rc = check_launch("flush_tc"))) return rc;
+    reduce_state_kernel<<<dim3(32, units), 256, 0, s>>>(*c, s_part, p_part, splits);
+    if ((rc = check_launch("reduce_state"))) return rc;
+  } else if (max_nf > 0) {
+    // cpc chunks per CTA: enough CTAs to cover the SMs
+    const int cpc = 4;
+    const int splits = (max_nf + cpc - 1) / cpc;
+    FlushArgs a{};
+    a.c = *c;
+    a.use_adapter = 0;
     a.ksrc = k;
     a.vsrc = v;
     a.k_unit = n_tok * D;
@@ -529,16 +993,10 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     a.v_c = 1;
     a.ring = 0;
     a.cpc = cpc;
-    a.s_out = s_part;
-    a.p_out = p_part;
     a.splits = splits;
     KVLC_CUDA(cudaFuncSetAttribute(flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FLUSH_SMEM));
     flush_kernel<<<dim3(splits, units), FLUSH_THREADS, FLUSH_SMEM, s>>>(a, seq);
     if ((rc = check_launch("flush"))) return rc;
-    if (use_ad) {
-      reduce_state_kernel<<<dim3(32, units), 256, 0, s>>>(*c, s_part, p_part, splits);
-      if ((rc = check_launch("reduce_state"))) return rc;
-    }
   }
   load_residual_kernel<<<dim3(64, units), 256, 0, s>>>(*c, k, v, n_tok, seq);
   set_lengths_kernel<<<1, 256, 0, s>>>(*c, seq);

@@ -4,7 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o umma_issue umma_issue.cu
 #include <cstdio>
 #include <cstdint>
-#include "kvlc_tc.cuh"
+#include "../../paper_2510_05373_b200/csrc/kvlc_tc.cuh"
 
 using namespace kvlc;
 

@@ -7,7 +7,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o umma_latency umma_latency.cu
 #include <cstdio>
 #include <cstdint>
-#include "kvlc_tc.cuh"
+#include "../../paper_2510_05373_b200/csrc/kvlc_tc.cuh"
 
 using namespace kvlc;
 
