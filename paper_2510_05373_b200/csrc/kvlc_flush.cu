@@ -478,12 +478,30 @@ struct FtSmem {
   uint8_t a[2][FT_TILE];     // A_phi (k_err, [M = token][K = channel]) then A_S (Phi^T, [M = feature][K = token])
   uint8_t bs[2][FT_TILE_S];  // B_S hi / lo: [K = token][N = 144]
   uint8_t codes[G * D];      // value codes [token][channel] (for the packed V words)
-  double2 kpar[D];           // per channel (min, scale) of the key chunk
+  double2 kpar[D];           // per channel (min, scale) of the key chunk (exact tie path)
+  float4 kparf[D];           // per channel (min, scale, 1 / scale) in fp32 (fast path)
   float red[2][FT_THREADS];
   uint64_t mphi, ms;
   uint32_t tbase;
 };
 
+// Value codes [token][channel] with an XOR swizzle on channel bits 2-4 (groups of 4
+// channels stay contiguous): conflict-free packing reads.
+__device__ __forceinline__ int vsw(int t, int ch) { return t * D + (ch ^ (((t ^ (t >> 3)) & 7) << 2)); }
+__device__ __forceinline__ uint32_t pack_v_word_sw(const uint8_t* codes, int wi) {  // pack_v_word on vsw
+  const int i = wi & 7, lane = (wi >> 3) & 31, w = wi >> 8;
+  const int g = lane >> 2, t0 = lane & 3, mt = i >> 2, p = i & 3;
+  const int toff[4] = {0, 1, 4, 5};
+  uint32_t word = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int t = 32 * w + 8 * t0 + 2 * mt + toff[q];
+      word |= (uint32_t)codes[vsw(t, 32 * p + 8 * j + g)] << (8 * q + 2 * j);
+    }
+  return word;
+}
 __device__ __forceinline__ int ft_off(int mn, int k) {  // byte offset of element (mn, k) in an MN-major tile
   return (mn & 7) * 2 + (k & 7) * 16 + (mn >> 3) * 2048 + (k >> 3) * 128;
 }
@@ -510,6 +528,18 @@ __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE],
           : "memory");
     }
 }
+
+#ifdef KVLC_TRACE
+__device__ long long g_ftrace[2][40][10];  // CTA (0, 0, h): per chunk clock64 at phase boundaries (thread 0)
+#define FT_STAMP(i)                                                                            \
+  do {                                                                                         \
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && it < 40) g_ftrace[h][it][i] = clock64(); \
+  } while (0)
+#else
+#define FT_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
 
 __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs a, const SeqInfo seq,
                                                                  const uint8_t* __restrict__ wtiles) {
@@ -556,10 +586,12 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     const uint16_t* K = a.ksrc + unit * a.k_unit + tok0 * a.k_t;
     const uint16_t* V = a.vsrc + unit * a.v_unit + tok0 * a.v_t;
     const size_t cb = (size_t)unit * c.max_chunks + ci;
+    FT_STAMP(0);
     if (it > 0) {  // the previous S GEMM has read A_S (aliased by A_phi) and B_S
       tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);
       tc::fence_after_sync();
     }
+    FT_STAMP(1);
 
     // ---- K1: keys, channel-wise.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3
     // (16-B vector loads).  Codes in fp32 with the exact fp64 decision near rounding
@@ -609,6 +641,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         const double mn = (double)mn16[0], mx = (double)mx16[0];
         const double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
         sm.kpar[ch0 + own] = make_double2(mn, scale);
+        sm.kparf[ch0 + own] = make_float4((float)mn, (float)scale, scale > 0.0 ? (float)(1.0 / scale) : 0.f, 0.f);
         if (writer) {
           c.kscale[cb * D + ch0 + own] = __half_as_ushort(__double2half(scale));
           c.kzero[cb * D + ch0 + own] = __half_as_ushort(__double2half(mn));
@@ -618,18 +651,21 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       uint32_t cw[4] = {0u, 0u, 0u, 0u};  // K words t0 = 0..3 of this lane's tokens
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const double2 pr = sm.kpar[ch0 + e];
-        const double mn = pr.x, scale = pr.y;
-        const float mnf = (float)mn, scf = (float)scale, invf = scale > 0.0 ? (float)(1.0 / scale) : 0.f;
+        const float4 pf = sm.kparf[ch0 + e];
+        const float mnf = pf.x, scf = pf.y, invf = pf.z;
         __half hi[4], lo[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           uint32_t code = 0u;
-          if (scale > 0.0) {
+          if (scf > 0.f) {
             const float q = (x[r][e] - mnf) * invf;
             const float fr = q - floorf(q);
-            if (fabsf(fr - 0.5f) < 1e-5f) code = code_of((double)x[r][e], mn, scale, 3);  // near a tie: exact
-            else code = (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f);
+            if (fabsf(fr - 0.5f) < 1e-5f) {  // near a tie: the exact fp64 decision
+              const double2 pr = sm.kpar[ch0 + e];
+              code = code_of((double)x[r][e], pr.x, pr.y, 3);
+            } else {
+              code = (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f);
+            }
           }
           ft_hilo(x[r][e] - fmaf((float)code, scf, mnf), hi[r], lo[r]);
           // byte q of word t0 holds channel 16kt + 2t0 + {0,8,1,9}[q]; bit pair r holds token 4l + r
@@ -646,9 +682,11 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = cw[t0];
       }
     }
+    FT_STAMP(2);
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
+    FT_STAMP(3);
     if (warp == 0) {  // phi GEMM: Z = k_err W_h
       tc::fence_after_sync();
       ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false);
@@ -659,10 +697,22 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     // The fp32 FWHT differs from the reference's fp64 dense x @ H in the last bits:
     // a token whose quotient lies near a rounding tie or whose scale / zero lies near
     // an fp16 rounding midpoint is re-evaluated in the reference's exact order.
-    for (int t = warp; t < G; t += FT_THREADS / 32) {
+    // rolling 8-deep register prefetch of this warp's 16 value rows (one 8-B piece per lane)
+    constexpr int VPF = 8, VTOK = G / (FT_THREADS / 32);
+    uint2 vpf[VPF];
+#pragma unroll
+    for (int i = 0; i < VPF; ++i)
+      vpf[i] = __ldg(reinterpret_cast<const uint2*>(V + (size_t)(warp + 8 * i) * a.v_t + lane * 4));
+#pragma unroll 1
+    for (int ti = 0; ti < VTOK; ++ti) {
+      const int t = warp + 8 * ti;
       float xf[4];
       {
-        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(V + (size_t)t * a.v_t + lane * 4));
+        uint2 raw = vpf[0];
+#pragma unroll
+        for (int i = 0; i < VPF - 1; ++i) vpf[i] = vpf[i + 1];
+        if (ti + VPF < VTOK)
+          vpf[VPF - 1] = __ldg(reinterpret_cast<const uint2*>(V + (size_t)(t + 8 * VPF) * a.v_t + lane * 4));
         xf[0] = __uint_as_float(raw.x << 16);
         xf[1] = __uint_as_float(raw.x & 0xffff0000u);
         xf[2] = __uint_as_float(raw.y << 16);
@@ -691,29 +741,32 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       }
       mnf = warp_min(mnf);
       mxf = warp_max(mxf);
-      double x[4], mn = (double)mnf, mx = (double)mxf;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) x[e] = (double)xf[e];
-      double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
-      double inv = scale > 0.0 ? 1.0 / scale : 0.0;
-      // fp32 FWHT error bound (7 add stages, the scaled result): a few ulps of the token's
-      // largest magnitude; the guards below are widened accordingly
-      const double big = fmax(fabs(mn), fabs(mx)), ferr = 4e-6 * big;
-      auto near_mid = [](double v, double rel) {  // fp16 rounding could differ from the fp64 reference value
-        return __half_as_ushort(__double2half(v * (1.0 - rel))) != __half_as_ushort(__double2half(v * (1.0 + rel)));
+      // Fast path in fp32.  fp32 FWHT error: a few ulps of the token's largest magnitude
+      // (ferr); a token is re-evaluated exactly when a quotient lies within qtol of a
+      // rounding tie or its zero / scale lies near an fp16 rounding midpoint (the stored
+      // metadata is float16 of the reference's fp64 value, cache.py:220-224).
+      const float range = mxf - mnf;
+      const float scf = range * (1.f / 3.f), invf = range > 0.f ? 3.f / range : 0.f;
+      const float ferr = 4e-6f * fmaxf(fabsf(mnf), fabsf(mxf));
+      auto near_mid = [](float v, float rel) {
+        return __half_as_ushort(__float2half_rn(v * (1.f - rel))) != __half_as_ushort(__float2half_rn(v * (1.f + rel)));
       };
-      bool amb = near_mid(mn, ferr / fmax(fabs(mn), 1e-30) + 1e-9) ||
-                 (scale > 0.0 && near_mid(scale, 2.0 * ferr / (mx - mn) + 1e-9));
-      const double qtol = 1e-5 + 4.0 * ferr * inv;
+      bool amb = near_mid(mnf, ferr / fmaxf(fabsf(mnf), 1e-30f) + 2e-7f) ||
+                 (range > 0.f && near_mid(scf, 2.f * ferr / range + 2e-7f));
+      const float qtol = 1e-4f + 4.f * ferr * invf;
+      uint32_t code[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const double r = __dsub_rn(x[e], mn) * inv;
-        amb |= scale > 0.0 && fabs(r - floor(r) - 0.5) < qtol;
+        const float q = (xf[e] - mnf) * invf;
+        amb |= range > 0.f && fabsf(q - floorf(q) - 0.5f) < qtol;
+        code[e] = range > 0.f ? (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f) : 0u;
       }
-      const double hs = 1.0 / sqrt((double)D);
+      float vmn = mnf, vsc = scf;
+      uint16_t meta_s = __half_as_ushort(__float2half_rn(scf)), meta_z = __half_as_ushort(__float2half_rn(mnf));
       if (__any_sync(0xffffffffu, amb)) {
         // fp64 FWHT: agrees with the dense fp64 x @ H to an ulp
-        double y[4];
+        const double hs = 1.0 / sqrt((double)D);
+        double x[4], y[4];
         {
           const uint2 raw = __ldg(reinterpret_cast<const uint2*>(V + (size_t)t * a.v_t + lane * 4));
           y[0] = (double)__uint_as_float(raw.x << 16);
@@ -734,8 +787,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
             y[e] = (lane & k) ? (o - y[e]) : (y[e] + o);
           }
         }
-        mn = INFINITY;
-        mx = -INFINITY;
+        double mn = INFINITY, mx = -INFINITY;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           x[e] = y[e] * hs;
@@ -744,8 +796,8 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         }
         mn = warp_min_d(mn);
         mx = warp_max_d(mx);
-        scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
-        inv = scale > 0.0 ? 1.0 / scale : 0.0;
+        double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
+        double inv = scale > 0.0 ? 1.0 / scale : 0.0;
         bool amb2 = near_half_tie(scale) || near_half_tie(mn);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -772,29 +824,38 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
           scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
           inv = scale > 0.0 ? 1.0 / scale : 0.0;
         }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) code[e] = code2(x[e], mn, scale, inv);
+        vmn = (float)mn;
+        vsc = (float)scale;
+        meta_s = __half_as_ushort(__double2half(scale));
+        meta_z = __half_as_ushort(__double2half(mn));
       }
       __half hi[4], lo[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const uint32_t code = code2(x[e], mn, scale, inv);
-        sm.codes[t * D + lane * 4 + e] = (uint8_t)code;
-        ft_hilo((float)__dadd_rn(__dmul_rn((double)code, scale), mn), hi[e], lo[e]);
+        ft_hilo(fmaf((float)code[e], vsc, vmn), hi[e], lo[e]);  // v_q (rotated basis)
       }
+      *reinterpret_cast<uint32_t*>(sm.codes + vsw(t, lane * 4)) = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
       // B_S element (token t, channel 4 lane + e): 4 consecutive channels are 8 contiguous bytes
       *reinterpret_cast<uint2*>(sm.bs[0] + ft_off(lane * 4, t)) = *reinterpret_cast<uint2*>(hi);
       *reinterpret_cast<uint2*>(sm.bs[1] + ft_off(lane * 4, t)) = *reinterpret_cast<uint2*>(lo);
       if (writer && lane == 0) {
-        c.vscale[cb * G + t] = __half_as_ushort(__double2half(scale));
-        c.vzero[cb * G + t] = __half_as_ushort(__double2half(mn));
+        c.vscale[cb * G + t] = meta_s;
+        c.vzero[cb * G + t] = meta_z;
       }
     }
+    FT_STAMP(4);
     __syncthreads();
+    FT_STAMP(5);
     if (writer)
-      for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word(sm.codes, wi);
+      for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word_sw(sm.codes, wi);
+    FT_STAMP(6);
 
     // ---- softmax of Z (token rows): warps w and w + 4 share TMEM lanes 32 (w & 3) .., 64 columns each ----
     tc::mbar_wait(&sm.mphi, (uint32_t)it & 1u);
     tc::fence_after_sync();
+    FT_STAMP(7);
     {
       const int t = 32 * (warp & 3) + lane, part = warp >> 2;
       float z[64];
@@ -806,12 +867,14 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       for (int i = 0; i < 64; ++i) m = fmaxf(m, z[i]);
       sm.red[part][t] = m;
       __syncthreads();
-      m = fmaxf(sm.red[0][t], sm.red[1][t]);
+      m = fmaxf(sm.red[0][t], sm.red[1][t]) * 1.4426950408889634f;
       float ssum = 0.f;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
-        z[i] = expf(z[i] - m);
-        ssum += z[i];
+        float e2;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(fmaf(z[i], 1.4426950408889634f, -m)));
+        z[i] = e2;
+        ssum += e2;
       }
       __syncthreads();
       sm.red[part][t] = ssum;
@@ -830,6 +893,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
+    FT_STAMP(8);
     if (warp == 0) {  // S GEMM: D_S += Phi^T [v_q | 1]
       tc::fence_after_sync();
       ft_gemm(tb + FT_COL_S, sm.a, sm.bs[0], sm.bs[1], FT_IDESC_S, it > 0);
@@ -880,6 +944,13 @@ __global__ void prep_wtiles_kernel(kvlc_adapter ad, int Hkv, uint8_t* __restrict
   }
 }
 
+#ifdef KVLC_TRACE
+}  // namespace
+int kvlc_ftrace_copy(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, g_ftrace, bytes < sizeof(g_ftrace) ? bytes : sizeof(g_ftrace)) == cudaSuccess ? 0 : 2;
+}
+namespace {
+#endif
 int check_cache(const kvlc_cache* c) {
   KVLC_REQUIRE(c != nullptr, "null cache descriptor");
   KVLC_REQUIRE(c->B >= 1 && c->Hkv >= 1 && c->Hq >= c->Hkv && c->Hq % c->Hkv == 0 &&
