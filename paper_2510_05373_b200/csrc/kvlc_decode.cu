@@ -496,20 +496,27 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
         w = m == -INFINITY ? 0.f : exp2f(m - M);
         den = fmaf(w, __ldcg(base + r * rstride + 1), den);
       }
-#pragma unroll 4
-      for (int i = 0; i < cnt; ++i) {
-        const float wi = __shfl_sync(0xffffffffu, w, i);
-        const float4 y = __ldcg(reinterpret_cast<const float4*>(base + (r0 + i) * rstride + 4) + lane);
-        if (r0 + i < a.nsq) {  // warp-uniform: quantized (rotated) vs residual (raw) basis
-          nr[0] = fmaf(wi, y.x, nr[0]);
-          nr[1] = fmaf(wi, y.y, nr[1]);
-          nr[2] = fmaf(wi, y.z, nr[2]);
-          nr[3] = fmaf(wi, y.w, nr[3]);
-        } else {
-          nw[0] = fmaf(wi, y.x, nw[0]);
-          nw[1] = fmaf(wi, y.y, nw[1]);
-          nw[2] = fmaf(wi, y.z, nw[2]);
-          nw[3] = fmaf(wi, y.w, nw[3]);
+      // batches of 8 records: all 8 loads in flight before the accumulation (long-context
+      // units have ~150 records per head)
+      for (int i0 = 0; i0 < cnt; i0 += 8) {
+        float4 y[8];
+        float wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u;
+          wv[u] = __shfl_sync(0xffffffffu, w, i & 31);
+          y[u] = i < cnt ? __ldcg(reinterpret_cast<const float4*>(base + (r0 + i) * rstride + 4) + lane)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u;
+          if (i >= cnt) break;
+          float* acc = r0 + i < a.nsq ? nr : nw;  // warp-uniform: quantized (rotated) vs residual (raw) basis
+          acc[0] = fmaf(wv[u], y[u].x, acc[0]);
+          acc[1] = fmaf(wv[u], y[u].y, acc[1]);
+          acc[2] = fmaf(wv[u], y[u].z, acc[2]);
+          acc[3] = fmaf(wv[u], y[u].w, acc[3]);
         }
       }
     }
@@ -539,7 +546,10 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
 // its unit's arrival counter after publishing its record; the last one
 // performs the LSE combine of the unit (no separate combine launch).
 template <int NG, int EXTRA>
-__global__ void __launch_bounds__(THREADS, 4) split_kernel(const DecArgs a) {
+#ifndef KVLC_SPLIT_MINB
+#define KVLC_SPLIT_MINB 4
+#endif
+__global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const DecArgs a) {
   __shared__ __align__(16) SplitSmem sm;
   __shared__ int last;
   const int U = a.c.B * a.c.Hkv;
@@ -629,8 +639,9 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   int span = std::max(0, std::min(maxc, chunk_hi) - chunk_lo);
   int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : 0;
   if (cpc == 0) {
-    // ~2 waves of quantized-split CTAs at 4 resident CTAs per SM
-    const long long ctas_wanted = 148LL * 4 * 2;
+    // ~2 waves of quantized-split CTAs at KVLC_SPLIT_MINB resident CTAs per SM
+    // (a wave-quantised cost model measured worse on configs 3 and 4)
+    const long long ctas_wanted = 148LL * KVLC_SPLIT_MINB * 2;
     const long long chunks = (long long)p.U * std::max(span, 1);
     cpc = (int)std::max(2LL, std::min(32LL, (chunks + ctas_wanted - 1) / ctas_wanted));
   }

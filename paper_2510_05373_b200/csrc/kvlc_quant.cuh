@@ -16,7 +16,10 @@
 //     the true max is tracked separately for literal-correction parity.
 #pragma once
 
-constexpr int STAGES = 3;
+#ifndef KVLC_STAGES
+#define KVLC_STAGES 3
+#endif
+constexpr int STAGES = KVLC_STAGES;
 constexpr float LAZY = 8.f;
 
 template <int NG>
