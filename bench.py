@@ -230,9 +230,84 @@ def run_ours(args, rank, world, local_rank):
     }
     if world == 1 and not args.no_fa:
         result["bf16_flash_attn"] = run_flash_attn(args, dev, step_ms)
+    if world == 1 and not args.no_extra:
+        del caches, graphs
+        torch.cuda.empty_cache()
+        result["other_configs"] = run_other_configs(dev, peak_gbs)
     if world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline_sample()
     return result
+
+
+def _time_decode(cache, q, bank, steps=20, warmup=5):
+    import torch
+    out = torch.empty_like(q)
+    for _ in range(warmup):
+        cache.decode(q, adapters=bank, out=out)
+    g = cache.capture_decode(q, adapters=bank, out=out)[0]
+    for _ in range(warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_other_configs(dev, peak_gbs):
+    """BASELINE configs 3-5 on this GPU (one point each; single cache, so config 4's
+    78 MB can be partly L2-resident -- stated).  Configs 3 / 4 time the same fused
+    decode step (CUDA graph); config 5 times kvlc_prefill (quantize/pack + FWHT +
+    adapter-state update) of Qwen3-8B shapes."""
+    import torch
+    from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache, flush_count
+    out = {}
+    for name, (b, hkv, hq, n) in {"config3_qwen2.5-7b_b16_ctx8k": (16, 4, 28, 8192),
+                                  "config4_llama3-8b_b1_ctx128k": (1, 8, 32, 131072)}.items():
+        bank = AdapterBank.initialize(hkv, device=dev)
+        c = BatchedKVCache(b, hkv, hq, n + 256, device=dev)
+        k = torch.randn(b, hkv, n, D, device=dev).bfloat16()
+        v = torch.randn(b, hkv, n, D, device=dev).bfloat16()
+        c.prefill(k, v, adapters=bank)
+        del k, v
+        q = torch.randn(b, hq, D, device=dev).bfloat16()
+        ms = _time_decode(c, q, bank)
+        nq = int(flush_count([n])[0]) * G
+        nbytes = algo_bytes_step(b, hkv, hq, nq, n - nq)
+        out[name] = {"us_per_step": ms * 1e3, "tokens_per_s": b / (ms * 1e-3),
+                     "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "roofline_frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs,
+                     "algorithmic_bytes": nbytes}
+        del c
+        torch.cuda.empty_cache()
+    # config 5: prefill of 32k tokens x 8 kv heads (Qwen3-8B attention shapes)
+    b, hkv, n = 1, 8, 32768
+    bank = AdapterBank.initialize(hkv, device=dev)
+    k = torch.randn(b, hkv, n, D, device=dev).bfloat16()
+    v = torch.randn(b, hkv, n, D, device=dev).bfloat16()
+    times = []
+    for i in range(4):
+        c = BatchedKVCache(b, hkv, 4 * hkv, n + 256, device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        c.prefill(k, v, adapters=bank)
+        e1.record()
+        torch.cuda.synchronize()
+        if i:
+            times.append(e0.elapsed_time(e1))
+        del c
+    ms = statistics.median(times)
+    nf = int(flush_count([n])[0])
+    nbytes = b * hkv * (2 * n * D * 2 + nf * (2 * G * D // 4 + 4 * D * 2) + (n - nf * G) * D * 2 * 2
+                        + (D * RANK + RANK) * 4)
+    out["config5_qwen3-8b_prefill_32k"] = {
+        "us_per_step": ms * 1e3, "kv_head_tokens_per_s": b * hkv * n / (ms * 1e-3),
+        "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "roofline_frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs,
+        "kernel": "flush_tc_kernel: tcgen05 3-pass fp16 phi_k / S,P GEMMs (TMEM accumulators)"}
+    return out
 
 
 def run_flash_attn(args, dev, ours_ms):
@@ -328,6 +403,7 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-fa", action="store_true", help="skip the bf16 FlashAttention comparison")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle sample")
+    ap.add_argument("--no-extra", action="store_true", help="skip BASELINE configs 3-5 (other_configs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
