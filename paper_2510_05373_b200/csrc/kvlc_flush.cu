@@ -123,6 +123,11 @@ struct FlushArgs {
   float* s_out;              // prefill: per-CTA S partial [units][splits][D][RANK]; null => cache S
   float* p_out;
   int splits;
+  // prefill tensor-core path: quant_kernel -> state kernel scratch, slot = unit * slot_stride + chunk
+  uint8_t* vbytes;           // [slot][G][D] value codes
+  float2* vsz;               // [slot][G] (scale, zero) fp32 per token
+  float2* ksz;               // [slot][D] (scale, zero) fp32 per channel
+  int slot_stride;
 };
 
 __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs a, const SeqInfo seq) {
@@ -477,9 +482,6 @@ struct FtSmem {
   uint8_t w[2][FT_TILE];     // W_h hi / lo: B of the phi GEMM, [K = channel][N = feature]
   uint8_t a[2][FT_TILE];     // A_phi (k_err, [M = token][K = channel]) then A_S (Phi^T, [M = feature][K = token])
   uint8_t bs[2][FT_TILE_S];  // B_S hi / lo: [K = token][N = 144]
-  uint8_t codes[G * D];      // value codes [token][channel] (for the packed V words)
-  double2 kpar[D];           // per channel (min, scale) of the key chunk (exact tie path)
-  float4 kparf[D];           // per channel (min, scale, 1 / scale) in fp32 (fast path)
   float red[2][FT_THREADS];
   uint64_t mphi, ms;
   uint32_t tbase;
@@ -529,70 +531,31 @@ __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE],
     }
 }
 
-#ifdef KVLC_TRACE
-__device__ long long g_ftrace[2][40][10];  // CTA (0, 0, h): per chunk clock64 at phase boundaries (thread 0)
-#define FT_STAMP(i)                                                                            \
-  do {                                                                                         \
-    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && it < 40) g_ftrace[h][it][i] = clock64(); \
-  } while (0)
-#else
-#define FT_STAMP(i) \
-  do {              \
-  } while (0)
+// Prefill quantization (K1 + K2) at one chunk per CTA: code decisions, FWHT,
+// packed words, fp16 metadata into the cache; fp32 scale / zero and the value
+// codes (bytes) into a scratch the tensor-core state kernel reconstructs k_err
+// and v_q from (cache.py:141-154).
+struct QkSmem {
+  uint8_t codes[G * D];  // value codes [token][channel] (swizzled, vsw)
+  double2 kpar[D];
+  float4 kparf[D];
+};
+#ifndef KVLC_QK_MINB
+#define KVLC_QK_MINB 2
 #endif
-
-__global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs a, const SeqInfo seq,
-                                                                 const uint8_t* __restrict__ wtiles) {
-  extern __shared__ __align__(1024) uint8_t ft_raw[];
-  FtSmem& sm = *reinterpret_cast<FtSmem*>(ft_raw);
+__global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const FlushArgs a, const SeqInfo seq) {
+  __shared__ __align__(16) QkSmem sm;
   const kvlc_cache& c = a.c;
-  const int unit = blockIdx.y, split = blockIdx.x, h = blockIdx.z;
-  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+  const int unit = blockIdx.y, ci = blockIdx.x;
+  const int b = unit / c.Hkv;
+  if (ci >= seq.nflush[b]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nf = seq.nflush[b];
-  const int c_lo = split * a.cpc, c_hi = min(nf, c_lo + a.cpc);
-  if (c_lo >= c_hi) return;
-  const bool writer = h == 0;  // the half-0 CTA stores codes and metadata
-
-  // resident W_h tiles (prepared by prep_wtiles_kernel), constant B_S columns, TMEM, barriers
-  {
-    const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + h) * 2 * FT_TILE);
-    uint4* dst = reinterpret_cast<uint4*>(sm.w[0]);
-    for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
-    tc::cp_commit();
-  }
-  for (int i = tid; i < 2 * G * 2; i += FT_THREADS) {  // tile x token x column group 16 / 17
-    const int tile = i / (2 * G), t = (i >> 1) % G, grp = 16 + (i & 1);
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (tile == 0 && grp == 16) v.x = 0x3C00u;  // hi tile, column 128 = 1.0 (P); lo and padding 0
-    *reinterpret_cast<uint4*>(sm.bs[tile] + grp * 2048 + (t >> 3) * 128 + (t & 7) * 16) = v;
-  }
-  if (warp == 0) tc::tmem_alloc(&sm.tbase, FT_TMEM);
-  if (tid == 0) {
-    tc::mbar_init(&sm.mphi, 1);
-    tc::mbar_init(&sm.ms, 1);
-    tc::mbar_fence_init();
-  }
-  tc::cp_wait<0>();
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tb = sm.tbase;
-  const uint32_t lane_addr = tb + ((uint32_t)(32 * (warp & 3)) << 16);
-
-  for (int ci = c_lo; ci < c_hi; ++ci) {
-    const int it = ci - c_lo;
-    const int64_t tok0 = (int64_t)ci * G;
-    const uint16_t* K = a.ksrc + unit * a.k_unit + tok0 * a.k_t;
-    const uint16_t* V = a.vsrc + unit * a.v_unit + tok0 * a.v_t;
-    const size_t cb = (size_t)unit * c.max_chunks + ci;
-    FT_STAMP(0);
-    if (it > 0) {  // the previous S GEMM has read A_S (aliased by A_phi) and B_S
-      tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);
-      tc::fence_after_sync();
-    }
-    FT_STAMP(1);
-
+  const bool writer = true;
+  const int64_t tok0 = (int64_t)ci * G;
+  const uint16_t* K = a.ksrc + unit * a.k_unit + tok0 * a.k_t;
+  const uint16_t* V = a.vsrc + unit * a.v_unit + tok0 * a.v_t;
+  const size_t cb = (size_t)unit * c.max_chunks + ci;
+  const size_t slot = (size_t)unit * a.slot_stride + ci;
     // ---- K1: keys, channel-wise.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3
     // (16-B vector loads).  Codes in fp32 with the exact fp64 decision near rounding
     // ties (quantize.py:202-207 bit-exact); the lane also packs the fragment-native
@@ -642,6 +605,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         const double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
         sm.kpar[ch0 + own] = make_double2(mn, scale);
         sm.kparf[ch0 + own] = make_float4((float)mn, (float)scale, scale > 0.0 ? (float)(1.0 / scale) : 0.f, 0.f);
+        a.ksz[slot * D + ch0 + own] = make_float2((float)scale, (float)mn);
         if (writer) {
           c.kscale[cb * D + ch0 + own] = __half_as_ushort(__double2half(scale));
           c.kzero[cb * D + ch0 + own] = __half_as_ushort(__double2half(mn));
@@ -653,7 +617,6 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       for (int e = 0; e < 16; ++e) {
         const float4 pf = sm.kparf[ch0 + e];
         const float mnf = pf.x, scf = pf.y, invf = pf.z;
-        __half hi[4], lo[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           uint32_t code = 0u;
@@ -667,14 +630,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
               code = (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f);
             }
           }
-          ft_hilo(x[r][e] - fmaf((float)code, scf, mnf), hi[r], lo[r]);
           // byte q of word t0 holds channel 16kt + 2t0 + {0,8,1,9}[q]; bit pair r holds token 4l + r
           const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
           cw[t0] |= code << (8 * qb + 2 * r);
         }
-        // A_phi element (token 4l + r, channel ch0 + e): 4 consecutive tokens are 8 contiguous bytes
-        *reinterpret_cast<uint2*>(sm.a[0] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(hi);
-        *reinterpret_cast<uint2*>(sm.a[1] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(lo);
       }
       if (writer) {
         const int wt = lane >> 3, g = lane & 7;  // tokens 32 wt + 4 g + r
@@ -682,17 +641,6 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = cw[t0];
       }
     }
-    FT_STAMP(2);
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    FT_STAMP(3);
-    if (warp == 0) {  // phi GEMM: Z = k_err W_h
-      tc::fence_after_sync();
-      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false);
-      tc::mma_commit_w(&sm.mphi);
-    }
-
     // ---- K2: values, FWHT post-rotation (fp32, guarded), token-wise quantization ----
     // The fp32 FWHT differs from the reference's fp64 dense x @ H in the last bits:
     // a token whose quotient lies near a rounding tie or whose scale / zero lies near
@@ -831,25 +779,177 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         meta_s = __half_as_ushort(__double2half(scale));
         meta_z = __half_as_ushort(__double2half(mn));
       }
-      __half hi[4], lo[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        ft_hilo(fmaf((float)code[e], vsc, vmn), hi[e], lo[e]);  // v_q (rotated basis)
-      }
-      *reinterpret_cast<uint32_t*>(sm.codes + vsw(t, lane * 4)) = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
-      // B_S element (token t, channel 4 lane + e): 4 consecutive channels are 8 contiguous bytes
-      *reinterpret_cast<uint2*>(sm.bs[0] + ft_off(lane * 4, t)) = *reinterpret_cast<uint2*>(hi);
-      *reinterpret_cast<uint2*>(sm.bs[1] + ft_off(lane * 4, t)) = *reinterpret_cast<uint2*>(lo);
+      const uint32_t cword = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
+      *reinterpret_cast<uint32_t*>(sm.codes + vsw(t, lane * 4)) = cword;
+      *reinterpret_cast<uint32_t*>(a.vbytes + ((size_t)slot * G + t) * D + lane * 4) = cword;  // state-kernel scratch
+      if (lane == 0) a.vsz[slot * G + t] = make_float2(vsc, vmn);
       if (writer && lane == 0) {
         c.vscale[cb * G + t] = meta_s;
         c.vzero[cb * G + t] = meta_z;
       }
     }
+  __syncthreads();
+  for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word_sw(sm.codes, wi);
+}
+
+#ifdef KVLC_TRACE
+__device__ long long g_ftrace[2][40][10];  // CTA (0, 0, h): per chunk clock64 at phase boundaries (thread 0)
+#define FT_STAMP(i)                                                                            \
+  do {                                                                                         \
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && it < 40) g_ftrace[h][it][i] = clock64(); \
+  } while (0)
+#else
+#define FT_STAMP(i) \
+  do {              \
+  } while (0)
+#endif
+
+__global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs a, const SeqInfo seq,
+                                                                 const uint8_t* __restrict__ wtiles) {
+  extern __shared__ __align__(1024) uint8_t ft_raw[];
+  FtSmem& sm = *reinterpret_cast<FtSmem*>(ft_raw);
+  const kvlc_cache& c = a.c;
+  const int unit = blockIdx.y, split = blockIdx.x, h = blockIdx.z;
+  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nf = seq.nflush[b];
+  const int c_lo = split * a.cpc, c_hi = min(nf, c_lo + a.cpc);
+  if (c_lo >= c_hi) return;
+
+  // resident W_h tiles (prepared by prep_wtiles_kernel), constant B_S columns, TMEM, barriers
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + h) * 2 * FT_TILE);
+    uint4* dst = reinterpret_cast<uint4*>(sm.w[0]);
+    for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
+    tc::cp_commit();
+  }
+  for (int i = tid; i < 2 * G * 2; i += FT_THREADS) {  // tile x token x column group 16 / 17
+    const int tile = i / (2 * G), t = (i >> 1) % G, grp = 16 + (i & 1);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (tile == 0 && grp == 16) v.x = 0x3C00u;  // hi tile, column 128 = 1.0 (P); lo and padding 0
+    *reinterpret_cast<uint4*>(sm.bs[tile] + grp * 2048 + (t >> 3) * 128 + (t & 7) * 16) = v;
+  }
+  if (warp == 0) tc::tmem_alloc(&sm.tbase, FT_TMEM);
+  if (tid == 0) {
+    tc::mbar_init(&sm.mphi, 1);
+    tc::mbar_init(&sm.ms, 1);
+    tc::mbar_fence_init();
+  }
+  tc::cp_wait<0>();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tb = sm.tbase;
+  const uint32_t lane_addr = tb + ((uint32_t)(32 * (warp & 3)) << 16);
+
+  uint4 kpre[8];  // raw keys of the next chunk (lane l: tokens 4l..4l+3, channels 16 warp..+15)
+  {
+    const uint16_t* K0 = a.ksrc + unit * a.k_unit + (int64_t)c_lo * G * a.k_t;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint4* src = reinterpret_cast<const uint4*>(K0 + (size_t)(4 * lane + r) * D + 16 * warp);
+      kpre[2 * r] = __ldg(src);
+      kpre[2 * r + 1] = __ldg(src + 1);
+    }
+  }
+  for (int ci = c_lo; ci < c_hi; ++ci) {
+    const int it = ci - c_lo;
+    const int64_t tok0 = (int64_t)ci * G;
+    const uint16_t* K = a.ksrc + unit * a.k_unit + tok0 * a.k_t;
+    const uint16_t* V = a.vsrc + unit * a.v_unit + tok0 * a.v_t;
+    const size_t cb = (size_t)unit * c.max_chunks + ci;
+    FT_STAMP(0);
+    if (it > 0) {  // the previous S GEMM has read A_S (aliased by A_phi) and B_S
+      tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);
+      tc::fence_after_sync();
+    }
+    FT_STAMP(1);
+
+    // ---- k_err = k - (s code + z) (cache.py:153) from the raw keys, the packed K words and the
+    // fp32 (scale, zero) of quant_kernel.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3.
+    {
+      const int ch0 = 16 * warp;
+      const size_t slot = (size_t)unit * a.slot_stride + ci;
+      float x[4][16];
+      uint4 kcur[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) kcur[i] = kpre[i];
+      if (ci + 1 < c_hi) {  // the next chunk's raw keys, in flight during this chunk
+        const uint16_t* Kn = K + (int64_t)G * a.k_t;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint4* src = reinterpret_cast<const uint4*>(Kn + (size_t)(4 * lane + r) * D + ch0);
+          kpre[2 * r] = __ldg(src);
+          kpre[2 * r + 1] = __ldg(src + 1);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint4 p0 = kcur[2 * r], p1 = kcur[2 * r + 1];
+        const uint32_t wv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          x[r][2 * e] = __uint_as_float(wv[e] << 16);
+          x[r][2 * e + 1] = __uint_as_float(wv[e] & 0xffff0000u);
+        }
+      }
+      uint32_t cw[4];
+      const int wt = lane >> 3, g = lane & 7;
+#pragma unroll
+      for (int t0 = 0; t0 < 4; ++t0) cw[t0] = __ldg(c.kcodes + cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp));
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float2 sz = __ldg(a.ksz + slot * D + ch0 + e);
+        const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
+        __half hi[4], lo[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float code = (float)((cw[t0] >> (8 * qb + 2 * r)) & 3u);
+          ft_hilo(x[r][e] - fmaf(code, sz.x, sz.y), hi[r], lo[r]);
+        }
+        // A_phi element (token 4l + r, channel ch0 + e): 4 consecutive tokens are 8 contiguous bytes
+        *reinterpret_cast<uint2*>(sm.a[0] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(hi);
+        *reinterpret_cast<uint2*>(sm.a[1] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(lo);
+      }
+    }
+    FT_STAMP(2);
+    tc::fence_proxy_async();
+    tc::fence_before_sync();
+    __syncthreads();
+    FT_STAMP(3);
+    if (warp == 0) {  // phi GEMM: Z = k_err W_h
+      tc::fence_after_sync();
+      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false);
+      tc::mma_commit_w(&sm.mphi);
+    }
+
+    // ---- v_q = s_t code + z_t (cache.py:154, rotated basis) -> B_S row t; thread t, half `part`
+    {
+      const int t = tid & 127, part = tid >> 7;
+      const size_t slot = (size_t)unit * a.slot_stride + ci;
+      const float2 sz = __ldg(a.vsz + slot * G + t);
+      const uint4* src = reinterpret_cast<const uint4*>(a.vbytes + (slot * G + t) * D + 64 * part);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 w = __ldg(src + q);
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {  // 8 channels 64 part + 16 q + 8 hh
+          __half hi[8], lo[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float code = (float)((wv[2 * hh + (e >> 2)] >> (8 * (e & 3))) & 0xffu);
+            ft_hilo(fmaf(code, sz.x, sz.y), hi[e], lo[e]);
+          }
+          const int ch = 64 * part + 16 * q + 8 * hh;
+          *reinterpret_cast<uint4*>(sm.bs[0] + ft_off(ch, t)) = *reinterpret_cast<uint4*>(hi);
+          *reinterpret_cast<uint4*>(sm.bs[1] + ft_off(ch, t)) = *reinterpret_cast<uint4*>(lo);
+        }
+      }
+    }
     FT_STAMP(4);
     __syncthreads();
     FT_STAMP(5);
-    if (writer)
-      for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word_sw(sm.codes, wi);
     FT_STAMP(6);
 
     // ---- softmax of Z (token rows): warps w and w + 4 share TMEM lanes 32 (w & 3) .., 64 columns each ----
@@ -980,9 +1080,11 @@ size_t kvlc_prefill_workspace(const kvlc_cache* c, int64_t n_tok) {
   int units = c->B * c->Hkv;
   int splits = (int)((nf + 3) / 4);
   if (splits < 1) splits = 1;
-  // S / P partials (the tensor-core path uses fewer splits) + the W hi / lo tiles
+  // S / P partials (the tensor-core path uses fewer splits) + the W hi / lo tiles +
+  // the quant_kernel -> state-kernel scratch (value codes, fp32 scale / zero)
   return align_up((size_t)units * splits * (D * RANK + RANK) * sizeof(float)) +
-         align_up((size_t)c->Hkv * 2 * 2 * FT_TILE);
+         align_up((size_t)c->Hkv * 2 * 2 * FT_TILE) + align_up((size_t)units * std::max<int64_t>(nf, 1) * G * D) +
+         2 * align_up((size_t)units * std::max<int64_t>(nf, 1) * G * sizeof(float2));
 }
 
 int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k, const uint16_t* v,
@@ -1021,7 +1123,11 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     Arena ar(ws, ws_bytes);
     float* s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
     uint8_t* wtiles = ar.take<uint8_t>((size_t)c->Hkv * 2 * 2 * FT_TILE);
-    KVLC_REQUIRE(s_part && wtiles, "prefill workspace too small (%zu bytes)", ws_bytes);
+    const int slot_stride = (int)std::max<int64_t>(1, n_tok / KVLC_G);
+    uint8_t* vbytes = ar.take<uint8_t>((size_t)units * slot_stride * G * D);
+    float2* vsz = ar.take<float2>((size_t)units * slot_stride * G);
+    float2* ksz = ar.take<float2>((size_t)units * slot_stride * D);
+    KVLC_REQUIRE(s_part && wtiles && vbytes && vsz && ksz, "prefill workspace too small (%zu bytes)", ws_bytes);
     float* p_part = s_part + (size_t)units * splits * D * RANK;
     KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
     prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
@@ -1042,6 +1148,12 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     a.s_out = s_part;
     a.p_out = p_part;
     a.splits = splits;
+    a.vbytes = vbytes;
+    a.vsz = vsz;
+    a.ksz = ksz;
+    a.slot_stride = slot_stride;
+    quant_kernel<<<dim3(max_nf, units), FT_THREADS, 0, s>>>(a, seq);
+    if ((rc = check_launch("quant"))) return rc;
     KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
     flush_tc_kernel<<<dim3(splits, units, 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
     if ((rc = check_launch("flush_tc"))) return rc;
