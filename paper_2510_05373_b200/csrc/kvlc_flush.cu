@@ -127,6 +127,7 @@ struct FlushArgs {
   uint8_t* vbytes;           // [slot][G][D] value codes
   float2* vsz;               // [slot][G] (scale, zero) fp32 per token
   float2* ksz;               // [slot][D] (scale, zero) fp32 per channel
+  uint4* kw;                 // [slot][8 warps][32 lanes] the lane's 4 packed K words (K1 fragment order)
   int slot_stride;
 };
 
@@ -483,9 +484,15 @@ struct FtSmem {
   uint8_t a[2][FT_TILE];     // A_phi (k_err, [M = token][K = channel]) then A_S (Phi^T, [M = feature][K = token])
   uint8_t bs[2][FT_TILE_S];  // B_S hi / lo: [K = token][N = 144]
   float red[2][FT_THREADS];
-  uint64_t mphi, ms;
+  // the chunk's quant_kernel outputs, bulk-copied one chunk ahead
+  uint4 kw[FT_THREADS];      // packed K words, one uint4 per (warp, lane)
+  float2 ksz[D];             // K (scale, zero) per channel
+  uint8_t vb[G * D];         // value codes [token][channel], 16 B chunks swizzled by token & 7
+  float2 vsz[G];             // V (scale, zero) per token
+  uint64_t mphi, ms, mpre;
   uint32_t tbase;
 };
+constexpr uint32_t FT_PRE_BYTES = FT_THREADS * 16 + D * 8 + G * D + G * 8;
 
 // Value codes [token][channel] with an XOR swizzle on channel bits 2-4 (groups of 4
 // channels stay contiguous): conflict-free packing reads.
@@ -513,10 +520,31 @@ __device__ __forceinline__ void ft_hilo(float x, __half& hi, __half& lo) {
 }
 __device__ __forceinline__ uint64_t ft_desc(const void* p) { return tc::bdesc(tc::smem_u32(p)); }
 
+// A tiles (A_phi = k_err [M = token][K = channel], A_S = Phi^T [M = feature][K = token]) in the
+// MN-major SWIZZLE_128B canonical layout: a 128 B row holds 64 MN elements of one K, 8 K rows
+// form a 1024 B atom whose 16 B chunks are XOR-ed with the row, K groups of 8 follow at 1024 B,
+// the second 64-wide MN block at 16 KB.  A warp storing one K for 128 MN (K1') or 8 MN for 32
+// K (softmax) hits every bank once per wavefront; the no-swizzle layout put one K of all
+// 8-wide MN groups in the same 4 banks (16-way conflicts).
+#ifndef KVLC_FT_LBO
+#define KVLC_FT_LBO 16384
+#endif
+#ifndef KVLC_FT_SBO
+#define KVLC_FT_SBO 1024
+#endif
+__device__ __forceinline__ int ft_off_a(int mn, int k) {
+  return (mn >> 6) * 16384 + (k >> 3) * 1024 + (k & 7) * 128 + ((((mn & 63) >> 3) ^ (k & 7)) << 4) + (mn & 7) * 2;
+}
+__device__ __forceinline__ uint64_t ft_desc_a(const void* p) {
+  return (uint64_t)((tc::smem_u32(p) >> 4) & 0x3fff) | ((uint64_t)(KVLC_FT_LBO >> 4) << 16) |
+         ((uint64_t)(KVLC_FT_SBO >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+constexpr int FT_A_KSTEP = 2048 >> 4;  // descriptor advance per K = 16 step (two 8-row groups)
+
 // 3 passes (hi*hi, hi*lo, lo*hi) of a K = 128 contraction: 24 MMAs, one elected lane.
 __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE], const uint8_t* b0, const uint8_t* b1,
                                         uint32_t idesc, bool accumulate) {
-  const uint64_t ah = ft_desc(a[0]), al = ft_desc(a[1]), bh = ft_desc(b0), bl = ft_desc(b1);
+  const uint64_t ah = ft_desc_a(a[0]), al = ft_desc_a(a[1]), bh = ft_desc(b0), bl = ft_desc(b1);
   const uint64_t pa[3] = {ah, ah, al}, pb[3] = {bh, bl, bh};
 #pragma unroll
   for (int p = 0; p < 3; ++p)
@@ -526,7 +554,7 @@ __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE],
       asm volatile(
           "{\n.reg .pred q, e;\nsetp.ne.b32 q, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
           "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(d),
-          "l"(pa[p] + 16 * j), "l"(pb[p] + 16 * j), "r"(idesc), "r"(acc)
+          "l"(pa[p] + FT_A_KSTEP * j), "l"(pb[p] + 16 * j), "r"(idesc), "r"(acc)
           : "memory");
     }
 }
@@ -640,6 +668,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
 #pragma unroll
         for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = cw[t0];
       }
+      a.kw[slot * 256 + tid] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
     }
     // ---- K2: values, FWHT post-rotation (fp32, guarded), token-wise quantization ----
     // The fp32 FWHT differs from the reference's fp64 dense x @ H in the last bits:
@@ -781,7 +810,8 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       }
       const uint32_t cword = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
       *reinterpret_cast<uint32_t*>(sm.codes + vsw(t, lane * 4)) = cword;
-      *reinterpret_cast<uint32_t*>(a.vbytes + ((size_t)slot * G + t) * D + lane * 4) = cword;  // state-kernel scratch
+      // state-kernel scratch: 16 B chunk (lane / 4) of row t stored at chunk (lane / 4) ^ (t & 7)
+      *reinterpret_cast<uint32_t*>(a.vbytes + ((size_t)slot * G + t) * D + ((((lane >> 2) ^ (t & 7)) << 4) | ((lane & 3) << 2))) = cword;
       if (lane == 0) a.vsz[slot * G + t] = make_float2(vsc, vmn);
       if (writer && lane == 0) {
         c.vscale[cb * G + t] = meta_s;
@@ -803,6 +833,14 @@ __device__ long long g_ftrace[2][40][10];  // CTA (0, 0, h): per chunk clock64 a
   do {              \
   } while (0)
 #endif
+
+__device__ __forceinline__ void ft_prefetch(FtSmem& sm, const FlushArgs& a, size_t slot) {
+  tc::mbar_expect_tx(&sm.mpre, FT_PRE_BYTES);
+  tc::bulk_g2s(sm.kw, a.kw + slot * FT_THREADS, FT_THREADS * 16, &sm.mpre);
+  tc::bulk_g2s(sm.ksz, a.ksz + slot * D, D * 8, &sm.mpre);
+  tc::bulk_g2s(sm.vb, a.vbytes + slot * G * D, G * D, &sm.mpre);
+  tc::bulk_g2s(sm.vsz, a.vsz + slot * G, G * 8, &sm.mpre);
+}
 
 __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs a, const SeqInfo seq,
                                                                  const uint8_t* __restrict__ wtiles) {
@@ -833,12 +871,15 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   if (tid == 0) {
     tc::mbar_init(&sm.mphi, 1);
     tc::mbar_init(&sm.ms, 1);
+    tc::mbar_init(&sm.mpre, 1);
     tc::mbar_fence_init();
+    ft_prefetch(sm, a, (size_t)unit * a.slot_stride + c_lo);
   }
   tc::cp_wait<0>();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  if ((tc::smem_u32(sm.a[0]) & 1023u) != 0) __trap();  // swizzle atoms must be 1024 B aligned
   const uint32_t tb = sm.tbase;
   const uint32_t lane_addr = tb + ((uint32_t)(32 * (warp & 3)) << 16);
 
@@ -863,6 +904,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);
       tc::fence_after_sync();
     }
+    tc::mbar_wait(&sm.mpre, (uint32_t)it & 1u);  // this chunk's staged quant_kernel outputs
     FT_STAMP(1);
 
     // ---- k_err = k - (s code + z) (cache.py:153) from the raw keys, the packed K words and the
@@ -893,13 +935,11 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
           x[r][2 * e + 1] = __uint_as_float(wv[e] & 0xffff0000u);
         }
       }
-      uint32_t cw[4];
-      const int wt = lane >> 3, g = lane & 7;
-#pragma unroll
-      for (int t0 = 0; t0 < 4; ++t0) cw[t0] = __ldg(c.kcodes + cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp));
+      const uint4 cwv = sm.kw[tid];
+      const uint32_t cw[4] = {cwv.x, cwv.y, cwv.z, cwv.w};
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        const float2 sz = __ldg(a.ksz + slot * D + ch0 + e);
+        const float2 sz = sm.ksz[ch0 + e];
         const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
         __half hi[4], lo[4];
 #pragma unroll
@@ -908,8 +948,8 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
           ft_hilo(x[r][e] - fmaf(code, sz.x, sz.y), hi[r], lo[r]);
         }
         // A_phi element (token 4l + r, channel ch0 + e): 4 consecutive tokens are 8 contiguous bytes
-        *reinterpret_cast<uint2*>(sm.a[0] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(hi);
-        *reinterpret_cast<uint2*>(sm.a[1] + ft_off(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(lo);
+        *reinterpret_cast<uint2*>(sm.a[0] + ft_off_a(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(hi);
+        *reinterpret_cast<uint2*>(sm.a[1] + ft_off_a(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(lo);
       }
     }
     FT_STAMP(2);
@@ -926,12 +966,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     // ---- v_q = s_t code + z_t (cache.py:154, rotated basis) -> B_S row t; thread t, half `part`
     {
       const int t = tid & 127, part = tid >> 7;
-      const size_t slot = (size_t)unit * a.slot_stride + ci;
-      const float2 sz = __ldg(a.vsz + slot * G + t);
-      const uint4* src = reinterpret_cast<const uint4*>(a.vbytes + (slot * G + t) * D + 64 * part);
+      const float2 sz = sm.vsz[t];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 w = __ldg(src + q);
+        const uint4 w = *reinterpret_cast<const uint4*>(sm.vb + t * D + (((4 * part + q) ^ (t & 7)) << 4));
         const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {  // 8 channels 64 part + 16 q + 8 hh
@@ -949,6 +987,10 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     }
     FT_STAMP(4);
     __syncthreads();
+    if (tid == 0 && ci + 1 < c_hi) {  // staging consumed by K1' / K2': fetch the next chunk's
+      tc::fence_proxy_async();
+      ft_prefetch(sm, a, (size_t)unit * a.slot_stride + ci + 1);
+    }
     FT_STAMP(5);
     FT_STAMP(6);
 
@@ -986,8 +1028,8 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         __half hi[8], lo[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) ft_hilo(z[f8 + e] * inv, hi[e], lo[e]);
-        *reinterpret_cast<uint4*>(sm.a[0] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(hi);
-        *reinterpret_cast<uint4*>(sm.a[1] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(lo);
+        *reinterpret_cast<uint4*>(sm.a[0] + ft_off_a(64 * part + f8, t)) = *reinterpret_cast<uint4*>(hi);
+        *reinterpret_cast<uint4*>(sm.a[1] + ft_off_a(64 * part + f8, t)) = *reinterpret_cast<uint4*>(lo);
       }
     }
     tc::fence_proxy_async();
@@ -1084,7 +1126,8 @@ size_t kvlc_prefill_workspace(const kvlc_cache* c, int64_t n_tok) {
   // the quant_kernel -> state-kernel scratch (value codes, fp32 scale / zero)
   return align_up((size_t)units * splits * (D * RANK + RANK) * sizeof(float)) +
          align_up((size_t)c->Hkv * 2 * 2 * FT_TILE) + align_up((size_t)units * std::max<int64_t>(nf, 1) * G * D) +
-         2 * align_up((size_t)units * std::max<int64_t>(nf, 1) * G * sizeof(float2));
+         2 * align_up((size_t)units * std::max<int64_t>(nf, 1) * G * sizeof(float2)) +
+         align_up((size_t)units * std::max<int64_t>(nf, 1) * FT_THREADS * 16);
 }
 
 int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k, const uint16_t* v,
@@ -1127,7 +1170,8 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     uint8_t* vbytes = ar.take<uint8_t>((size_t)units * slot_stride * G * D);
     float2* vsz = ar.take<float2>((size_t)units * slot_stride * G);
     float2* ksz = ar.take<float2>((size_t)units * slot_stride * D);
-    KVLC_REQUIRE(s_part && wtiles && vbytes && vsz && ksz, "prefill workspace too small (%zu bytes)", ws_bytes);
+    uint4* kw = ar.take<uint4>((size_t)units * slot_stride * FT_THREADS);
+    KVLC_REQUIRE(s_part && wtiles && vbytes && vsz && ksz && kw, "prefill workspace too small (%zu bytes)", ws_bytes);
     float* p_part = s_part + (size_t)units * splits * D * RANK;
     KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
     prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
@@ -1151,6 +1195,7 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     a.vbytes = vbytes;
     a.vsz = vsz;
     a.ksz = ksz;
+    a.kw = kw;
     a.slot_stride = slot_stride;
     quant_kernel<<<dim3(max_nf, units), FT_THREADS, 0, s>>>(a, seq);
     if ((rc = check_launch("quant"))) return rc;

@@ -1,0 +1,2 @@
+bash tools/run_pfv.sh "$@"
+KVLC_LIB=tools/_trace/libkvlinc.so python tools/trace_prefill.py | head -8
