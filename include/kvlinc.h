@@ -248,6 +248,48 @@ int kvlc_export_chunk(const kvlc_cache* cache, int32_t unit, int32_t chunk,
                       uint16_t* kzero, uint16_t* vscale, uint16_t* vzero,
                       void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* standalone blocks (bf16 in, serving formats out) for callers with their   */
+/* own K / V storage; codes are bit-identical to quantize_tensor on the same  */
+/* bf16 values, fp16 scale / zero = float16(reference float64 value).         */
+/* ------------------------------------------------------------------------ */
+
+/* quantize_tensor (quantize.py:220-239) on x bf16 [rows][ld] (first `cols`
+ * columns): token axis -> words [rows][ceil(cols/L)], scale/zero
+ * [rows][ceil(cols/G)]; channel axis (a key chunk, cache.py:141) -> words
+ * [ceil(rows/L)][cols], scale/zero [ceil(rows/G)][cols] (f16).  err_opt
+ * (may be NULL): float [rows][cols] = x - dequantize (k_err, cache.py:153). */
+int kvlc_quantize_pack(const uint16_t* x, int64_t rows, int64_t cols, int64_t ld,
+                       int axis, int bits, int group, uint32_t* words,
+                       uint16_t* scale, uint16_t* zero, float* err_opt,
+                       void* stream);
+
+/* Value path of flush_group (cache.py:143-145): rotate(x, H, "post")
+ * (hadamard.py:45-57) of bf16 rows [rows][ld] (dim a power of two), then
+ * token-wise quantization: words [rows][ceil(dim/L)], scale/zero
+ * [rows][ceil(dim/G)] f16; vq_opt (may be NULL): float [rows][dim] = the
+ * dequantized rotated values (v_q, cache.py:154). */
+size_t kvlc_fwht_quantize_workspace(int64_t rows, int dim);
+int kvlc_fwht_quantize_pack(const uint16_t* x, int64_t rows, int dim, int64_t ld,
+                            int bits, int group, uint32_t* words,
+                            uint16_t* scale, uint16_t* zero, float* vq_opt,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* Adapter-state update of flush_group (cache.py:155-158) for n tokens:
+ * S [d][rank] += sum_i outer(vq_rot[i], phi_k(k_err[i])), P [rank] +=
+ * sum_i phi_k(k_err[i]); k_err, vq_rot float [n][d], W1k / W2k float
+ * [d][rank/2] (adapter.py:80-96); float64 arithmetic, fp32 state. */
+size_t kvlc_state_update_workspace(int64_t n, int rank);
+int kvlc_state_update(const float* k_err, const float* vq_rot, int64_t n, int d,
+                      int rank, const float* w1k, const float* w2k, float* S,
+                      float* P, void* ws, size_t ws_bytes, void* stream);
+
+/* flush_group (cache.py:132-158) on every sequence b with flush_host[b] != 0
+ * (residual length >= R + G), without appending: the fused K1+K2+K3 kernel. */
+int kvlc_flush_due(const kvlc_cache* cache, const kvlc_adapter* ad,
+                   const int32_t* flush_host, void* ws, size_t ws_bytes,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

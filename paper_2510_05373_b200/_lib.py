@@ -82,6 +82,16 @@ _SIGS = {
                                    c_int32, c_void_p, c_void_p]),
     "kvlc_export_chunk": (c_int, [POINTER(KvlcCache), c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
+    "kvlc_quantize_pack": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_int, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p]),
+    "kvlc_fwht_quantize_workspace": (c_size_t, [c_int64, c_int]),
+    "kvlc_fwht_quantize_pack": (c_int, [c_void_p, c_int64, c_int, c_int64, c_int, c_int, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "kvlc_state_update_workspace": (c_size_t, [c_int64, c_int]),
+    "kvlc_state_update": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "kvlc_flush_due": (c_int, [POINTER(KvlcCache), POINTER(KvlcAdapter), POINTER(c_int32), c_void_p,
+                               c_size_t, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -177,14 +177,18 @@ class BatchedKVCache:
         self.res_len[:] = lens - nf * G
 
     def append(self, k_t: torch.Tensor, v_t: torch.Tensor, adapters: AdapterBank | None = None,
-               active=None):
+               active=None, defer_flush: bool = False):
         """Append one token per (active) sequence: k_t, v_t bf16 [B, Hkv, 128].
-        A sequence whose window reaches R + G flushes its oldest G tokens."""
+        A sequence whose window reaches R + G flushes its oldest G tokens, unless
+        `defer_flush` (the caller then runs `flush_due()` before that sequence's
+        next append, e.g. to batch flushes off the decode step)."""
         if k_t.shape != (self.B, self.Hkv, D) or v_t.shape != k_t.shape:
             raise ValueError(f"token dims {tuple(k_t.shape)}/{tuple(v_t.shape)} != ({self.B}, {self.Hkv}, {D})")
         act = np.ones(self.B, bool) if active is None else np.asarray(active, bool)
         new_len = self.res_len + act
-        flush = act & (new_len == R + G)
+        if np.any(new_len > SLOTS):
+            raise ValueError("residual window full: run flush_due() before appending")
+        flush = act & (new_len == R + G) & (not defer_flush)
         if np.any(self.n_chunks + flush > self.max_chunks):
             raise ValueError(f"append exceeds capacity of {self.max_tokens} tokens")
         ad = _adapter_struct(adapters)
@@ -268,6 +272,22 @@ class BatchedKVCache:
         return rec, corr
 
     # ------------------------------------------------------------------ export
+    def flush_due(self, adapters: AdapterBank | None = None) -> np.ndarray:
+        """flush_group (cache.py:132-158) on every sequence whose window holds
+        R + G tokens (deferred appends); returns the flushed sequence mask."""
+        flush = self.res_len >= R + G
+        if not np.any(flush):
+            return flush
+        if np.any(self.n_chunks + flush > self.max_chunks):
+            raise ValueError(f"flush exceeds capacity of {self.max_tokens} tokens")
+        f_c = (ctypes.c_int32 * self.B)(*flush.astype(np.int32).tolist())
+        _lib.call("kvlc_flush_due", ctypes.byref(self._struct), ctypes.byref(_adapter_struct(adapters)), f_c,
+                  None, 0, _lib.stream_handle())
+        self.res_len = self.res_len - flush * G
+        self.res_start = np.where(flush, (self.res_start + G) % SLOTS, self.res_start)
+        self.n_chunks = self.n_chunks + flush
+        return flush
+
     def export_chunk(self, b: int, kvh: int, chunk: int) -> dict:
         """One quantized chunk in the reference layout (channel-axis key words
         (8, 128), value_rows words (128, 8), fp16 metadata)."""
