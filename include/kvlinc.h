@@ -248,6 +248,22 @@ int kvlc_export_chunk(const kvlc_cache* cache, int32_t unit, int32_t chunk,
                       uint16_t* kzero, uint16_t* vscale, uint16_t* vzero,
                       void* stream);
 
+/* .kvlc image of one (b, kv-head) unit (serialize_cache / deserialize_cache,
+ * cache.py:197-307): the reference's little-endian per-head format — header
+ * "KVLC" + 9 u32, key / value code words in the reference layouts, f16
+ * metadata, f16 residual (oldest first) and f16 S / P (rank 0 = no states).
+ * `image` is a device buffer of kvlc_unit_image_bytes() bytes (0 = invalid
+ * arguments).  The host mirrors the sequence counters and passes them.
+ * Deserialization loads the residual at ring slot 0 (rounded f16 -> bf16) and
+ * sets the counters of sequence unit / Hkv (all its units must agree). */
+size_t kvlc_unit_image_bytes(int32_t n_chunks, int32_t res_len, int32_t rank);
+int kvlc_serialize_unit(const kvlc_cache* cache, int32_t unit, int32_t n_chunks,
+                        int32_t res_start, int32_t res_len, int32_t rank,
+                        uint8_t* image, void* stream);
+int kvlc_deserialize_unit(const kvlc_cache* cache, int32_t unit,
+                          const uint8_t* image, int32_t n_chunks,
+                          int32_t res_len, int32_t rank, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* standalone blocks (bf16 in, serving formats out) for callers with their   */
 /* own K / V storage; codes are bit-identical to quantize_tensor on the same  */

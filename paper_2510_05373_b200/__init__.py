@@ -14,7 +14,8 @@ is `paper_2510_05373_b200.batched` / `.distributed`.
 from .adapter import (CorrectionAdapter, correction_term, feature_map, phi_k, phi_q,  # noqa: F401
                       rng)
 from .attention import DecodePartial, decode_step_blocked  # noqa: F401
-from .cache import FootprintReport, KVCacheState, memory_footprint  # noqa: F401
+from .cache import (CacheFormatError, FootprintReport, KVCacheState, deserialize_cache,  # noqa: F401
+                    memory_footprint, read_cache, serialize_cache, write_cache)
 from .hadamard import HadamardMatrix, hadamard_matrix, rotate  # noqa: F401
 from .quantize import (QuantConfig, QuantizedTensor, dequantize_group,  # noqa: F401
                        expected_quant_mse, pack_codes, quantize_group, quantize_tensor,
@@ -25,7 +26,8 @@ __version__ = "1.0.0"
 __all__ = [
     "CorrectionAdapter", "correction_term", "feature_map", "phi_q", "phi_k", "rng",
     "DecodePartial", "decode_step_blocked",
-    "FootprintReport", "KVCacheState", "memory_footprint",
+    "FootprintReport", "KVCacheState", "memory_footprint", "serialize_cache", "deserialize_cache",
+    "read_cache", "write_cache", "CacheFormatError",
     "HadamardMatrix", "hadamard_matrix", "rotate",
     "QuantConfig", "QuantizedTensor", "dequantize_group", "expected_quant_mse", "pack_codes",
     "quantize_group", "quantize_tensor", "unpack_codes",

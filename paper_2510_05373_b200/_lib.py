@@ -82,6 +82,11 @@ _SIGS = {
                                    c_int32, c_void_p, c_void_p]),
     "kvlc_export_chunk": (c_int, [POINTER(KvlcCache), c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
+    "kvlc_unit_image_bytes": (c_size_t, [c_int32, c_int32, c_int32]),
+    "kvlc_serialize_unit": (c_int, [POINTER(KvlcCache), c_int32, c_int32, c_int32, c_int32, c_int32, c_void_p,
+                                    c_void_p]),
+    "kvlc_deserialize_unit": (c_int, [POINTER(KvlcCache), c_int32, c_void_p, c_int32, c_int32, c_int32,
+                                      c_void_p]),
     "kvlc_quantize_pack": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_int, c_void_p,
                                    c_void_p, c_void_p, c_void_p, c_void_p]),
     "kvlc_fwht_quantize_workspace": (c_size_t, [c_int64, c_int]),

@@ -24,6 +24,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import kvlc_format as fmt
 from ._lib import D, G, R, RANK, SLOTS, KvlcAdapter, KvlcCache, KvlcDecodeOpts
 from .adapter import CorrectionAdapter
 
@@ -74,6 +75,10 @@ def flush_count(lens, keep_window: bool = True) -> np.ndarray:
     return lens // G
 
 
+def _adapters_on(adapters) -> bool:
+    return adapters is not None and bool(adapters.enabled)
+
+
 def _adapter_struct(adapters):
     if adapters is None:
         return KvlcAdapter(None, None, None, None, 0)
@@ -115,6 +120,9 @@ class BatchedKVCache:
         self.n_chunks = np.zeros(batch, np.int64)
         self.res_start = np.zeros(batch, np.int64)
         self.res_len = np.zeros(batch, np.int64)
+        # adapter_rank of each sequence's states (cache.py:160-166): RANK after
+        # its first flush with an enabled adapter, else 0 (no S / P in .kvlc)
+        self.state_rank = np.zeros(batch, np.int64)
         self._ws = None
         self._struct = self._make_struct()
 
@@ -172,6 +180,8 @@ class BatchedKVCache:
         _lib.call("kvlc_prefill", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(k), _ptr(v), n,
                   lens_c, int(bool(keep_window)), _ptr(ws), ws.numel(), _lib.stream_handle())
         nf = flush_count(lens, keep_window)
+        if _adapters_on(adapters):
+            self.state_rank[nf > 0] = RANK
         self.n_chunks[:] = nf
         self.res_start[:] = 0
         self.res_len[:] = lens - nf * G
@@ -198,6 +208,8 @@ class BatchedKVCache:
         v_t = v_t.to(self.device, torch.bfloat16).contiguous()
         _lib.call("kvlc_append", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
                   a_c, f_c, None, 0, _lib.stream_handle())
+        if _adapters_on(adapters):
+            self.state_rank[flush] = RANK
         self.res_len = new_len - flush * G
         self.res_start = np.where(flush, (self.res_start + G) % SLOTS, self.res_start)
         self.n_chunks = self.n_chunks + flush
@@ -283,10 +295,53 @@ class BatchedKVCache:
         f_c = (ctypes.c_int32 * self.B)(*flush.astype(np.int32).tolist())
         _lib.call("kvlc_flush_due", ctypes.byref(self._struct), ctypes.byref(_adapter_struct(adapters)), f_c,
                   None, 0, _lib.stream_handle())
+        if _adapters_on(adapters):
+            self.state_rank[flush] = RANK
         self.res_len = self.res_len - flush * G
         self.res_start = np.where(flush, (self.res_start + G) % SLOTS, self.res_start)
         self.n_chunks = self.n_chunks + flush
         return flush
+
+    # ------------------------------------------------------------------ .kvlc I/O
+    def serialize(self, b: int, kvh: int) -> bytes:
+        """The reference's .kvlc bytes (serialize_cache, cache.py:209-230) of the
+        per-head cache (b, kvh), written on the device in one kernel."""
+        n, start, n_res, rank = (int(self.n_chunks[b]), int(self.res_start[b]), int(self.res_len[b]),
+                                 int(self.state_rank[b]))
+        lib = _lib.load()
+        img = torch.empty(lib.kvlc_unit_image_bytes(n, n_res, rank), dtype=torch.uint8, device=self.device)
+        _lib.call("kvlc_serialize_unit", ctypes.byref(self._struct), b * self.Hkv + kvh, n, start, n_res, rank,
+                  _ptr(img), _lib.stream_handle())
+        return img.cpu().numpy().tobytes()
+
+    def load(self, b: int, images) -> None:
+        """Load sequence b from one .kvlc image per kv head (deserialize_cache,
+        cache.py:252-307).  The images must describe the serving format (d = G =
+        R = 128, 2 bits, rotated values, rank 0 or 256) and agree on their token
+        counts; the residual is stored at bf16 (the serving window precision)."""
+        if len(images) != self.Hkv:
+            raise ValueError(f"need {self.Hkv} images (one per kv head), got {len(images)}")
+        hdrs = [fmt.parse_header(im) for im in images]
+        for im, h in zip(images, hdrs):
+            fmt.split(im, h)  # truncation / trailing-byte checks
+            want = (D, G, R, 2, 1)
+            got = (h.head_dim, h.group, h.window, h.bits, h.rotated)
+            if got != want:
+                raise ValueError(f"cache format (head_dim, group_size, residual_window, bits, rotated) = {got}; "
+                                 f"the serving cache holds {want}")
+            if h.rank not in (0, RANK):
+                raise ValueError(f"adapter rank {h.rank} != cache state rank {RANK}")
+        if len({(h.n_q, h.n_res, h.rank) for h in hdrs}) != 1:
+            raise ValueError("kv-head images of one sequence disagree on token counts or state rank")
+        h = hdrs[0]
+        n = h.n_q // G
+        if n > self.max_chunks or h.n_res > SLOTS:
+            raise ValueError(f"cache of {h.n_q + h.n_res} tokens exceeds capacity of {self.max_tokens} tokens")
+        for kvh, im in enumerate(images):
+            dev = torch.frombuffer(bytearray(im), dtype=torch.uint8).to(self.device)
+            _lib.call("kvlc_deserialize_unit", ctypes.byref(self._struct), b * self.Hkv + kvh, _ptr(dev), n,
+                      h.n_res, h.rank, _lib.stream_handle())
+        self.n_chunks[b], self.res_start[b], self.res_len[b], self.state_rank[b] = n, 0, h.n_res, h.rank
 
     def export_chunk(self, b: int, kvh: int, chunk: int) -> dict:
         """One quantized chunk in the reference layout (channel-axis key words

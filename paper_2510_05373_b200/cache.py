@@ -22,7 +22,11 @@ from . import _lib
 from ._device import empty_dev, to_dev, to_host, zeros_dev
 from .adapter import CorrectionAdapter
 from .hadamard import hadamard_matrix
+from .kvlc_format import VERSION, CacheFormatError, Header, join, parse_header, split
 from .quantize import QuantConfig, QuantizedTensor, _lanes
+
+__all__ = ["FootprintReport", "KVCacheState", "memory_footprint", "serialize_cache", "deserialize_cache",
+           "write_cache", "read_cache", "CacheFormatError"]
 
 
 @dataclass
@@ -281,3 +285,70 @@ def memory_footprint(cache: KVCacheState) -> FootprintReport:
     states = 2 * (d * cache.adapter_rank + cache.adapter_rank) if cache.adapter_rank else 0
     return FootprintReport(packed_codes=4 * code_words, scales_zeros=2 * 2 * groups,
                            residual=2 * 2 * cache.residual_len * d, correction_states=states)
+
+
+# -- serialization (cache.py:197-307) ------------------------------------------
+
+def serialize_cache(cache: KVCacheState) -> bytes:
+    """The reference's .kvlc bytes for one per-head cache (cache.py:209-230)."""
+    n, d = cache._n_chunks, cache.head_dim
+    h = Header(VERSION, d, cache.adapter_rank, cache.group_size, cache.residual_window,
+               cache.config_k.bits, int(cache.values_rotated), cache.quantized_tokens, cache.residual_len)
+    parts = {"res_k": cache.residual_keys(), "res_v": cache.residual_values()}
+    if n:
+        chunks = cache.key_chunks
+        vr = cache.value_rows
+        parts["kcodes"] = np.stack([c.codes for c in chunks])
+        parts["kmeta"] = np.stack([np.stack([c.scales, c.zeros]) for c in chunks])
+        parts.update(vcodes=vr.codes, vscales=vr.scales, vzeros=vr.zeros)
+    else:
+        for name, dt, shape in h.sections():
+            parts.setdefault(name, np.zeros(shape))
+    if cache.adapter_rank:
+        parts["s"], parts["p"] = cache.s_state, cache.p_state
+    return join(h, parts)
+
+
+def deserialize_cache(data: bytes) -> KVCacheState:
+    """Rebuild a per-head cache from .kvlc bytes (cache.py:252-307); the 16-bit
+    fields come back as float64."""
+    data = bytes(data)
+    h = parse_header(data)
+    cache = KVCacheState(h.head_dim, bits=h.bits, group_size=h.group, residual_window=h.window,
+                         rotate_values=bool(h.rotated))
+    sec = split(data, h)
+    if h.n_res > h.window + h.group:
+        raise CacheFormatError(f"residual length {h.n_res} exceeds window + group "
+                               f"{h.window + h.group}")
+    st = cache._storage()
+    f64 = lambda a: np.asarray(a, np.float64)
+    n = h.n_q // h.group
+    if n:
+        st["kwords"] = to_dev(np.ascontiguousarray(sec["kcodes"]).view(np.uint32).astype(np.uint32))
+        st["kscales"] = to_dev(f64(sec["kmeta"][:, 0, 0]))
+        st["kzeros"] = to_dev(f64(sec["kmeta"][:, 1, 0]))
+        st["vwords"] = to_dev(np.ascontiguousarray(sec["vcodes"]).astype(np.uint32))
+        st["vscales"] = to_dev(f64(sec["vscales"]))
+        st["vzeros"] = to_dev(f64(sec["vzeros"]))
+    if h.n_res:
+        st["res_k"][: h.n_res] = to_dev(f64(sec["res_k"]))
+        st["res_v"][: h.n_res] = to_dev(f64(sec["res_v"]))
+    if h.rank:
+        cache.adapter_rank = h.rank
+        st["s"] = to_dev(f64(sec["s"]))
+        st["p"] = to_dev(f64(sec["p"]))
+    cache._n_chunks, cache._res_len = n, h.n_res
+    cache.tokens_total = h.n_q + h.n_res
+    return cache
+
+
+def write_cache(cache: KVCacheState, path):
+    """cache.py:310-312."""
+    with open(path, "wb") as fh:
+        fh.write(serialize_cache(cache))
+
+
+def read_cache(path) -> KVCacheState:
+    """cache.py:315-317."""
+    with open(path, "rb") as fh:
+        return deserialize_cache(fh.read())

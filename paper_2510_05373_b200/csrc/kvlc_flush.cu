@@ -457,6 +457,143 @@ __global__ void export_chunk_kernel(kvlc_cache c, int unit, int chunk, uint32_t*
 }
 
 // ---------------------------------------------------------------------------
+// .kvlc image of one unit (cache.py:197-230, little-endian): header "KVLC" + u32
+// (version 1, d, rank, G, R, bits, values_rotated, quantized_tokens, residual_len);
+// key chunk words [8][128] per chunk; value_rows words [n_q][8]; per chunk key
+// scales then zeros (f16 [128]); value scales [n_q] then zeros [n_q] (f16);
+// residual keys then values (f16 [n_res][128], oldest first); S [128][256] then
+// P [256] (f16) when rank > 0.  Offsets for n chunks / n_res residual tokens:
+struct ImageLayout {
+  size_t kcodes, vcodes, kmeta, vscale, vzero, rk, rv, S, P, end;
+  __host__ __device__ ImageLayout(int n, int n_res, int rank) {
+    kcodes = 40;
+    vcodes = kcodes + (size_t)n * 8 * 128 * 4;
+    kmeta = vcodes + (size_t)n * G * 8 * 4;
+    vscale = kmeta + (size_t)n * 2 * D * 2;
+    vzero = vscale + (size_t)n * G * 2;
+    rk = vzero + (size_t)n * G * 2;
+    rv = rk + (size_t)n_res * D * 2;
+    S = rv + (size_t)n_res * D * 2;
+    P = S + (rank ? (size_t)D * rank * 2 : 0);
+    end = P + (size_t)rank * 2;
+  }
+};
+
+// grid: n chunk blocks, then one residual / header block, then state blocks.
+__global__ void serialize_unit_kernel(kvlc_cache c, int unit, int n, int res_start, int n_res, int rank,
+                                      uint8_t* __restrict__ img) {
+  const ImageLayout L(n, n_res, rank);
+  const int bx = blockIdx.x, tid = threadIdx.x;
+  if (bx < n) {
+    const size_t cb = (size_t)unit * c.max_chunks + bx;
+    const uint32_t* kwords = c.kcodes + cb * 1024;
+    const uint32_t* vwords = c.vcodes + cb * 1024;
+    uint32_t* kw = reinterpret_cast<uint32_t*>(img + L.kcodes) + (size_t)bx * 1024;
+    uint32_t* vw = reinterpret_cast<uint32_t*>(img + L.vcodes) + (size_t)bx * G * 8;
+    for (int i = tid; i < 1024; i += blockDim.x) {
+      const int w = i / 128, ch = i % 128, t = i / 8, j = i % 8;
+      uint32_t kword = 0, vword = 0;
+      for (int l = 0; l < 16; ++l) {
+        kword |= k_code(kwords, 16 * w + l, ch) << (2 * l);
+        vword |= v_code(vwords, t, 16 * j + l) << (2 * l);
+      }
+      kw[i] = kword;
+      vw[i] = vword;
+    }
+    uint16_t* km = reinterpret_cast<uint16_t*>(img + L.kmeta) + (size_t)bx * 2 * D;
+    uint16_t* vs = reinterpret_cast<uint16_t*>(img + L.vscale) + (size_t)bx * G;
+    uint16_t* vz = reinterpret_cast<uint16_t*>(img + L.vzero) + (size_t)bx * G;
+    for (int i = tid; i < 128; i += blockDim.x) {
+      km[i] = c.kscale[cb * D + i];
+      km[D + i] = c.kzero[cb * D + i];
+      vs[i] = c.vscale[cb * G + i];
+      vz[i] = c.vzero[cb * G + i];
+    }
+  } else if (bx == n) {
+    if (tid == 0) {
+      const uint32_t hdr[10] = {0x434C564Bu /* "KVLC" */, 1u, (uint32_t)D, (uint32_t)rank, (uint32_t)G, (uint32_t)KVLC_R,
+                                2u, 1u, (uint32_t)(n * G), (uint32_t)n_res};
+      for (int i = 0; i < 10; ++i) reinterpret_cast<uint32_t*>(img)[i] = hdr[i];
+    }
+    uint16_t* rk = reinterpret_cast<uint16_t*>(img + L.rk);
+    uint16_t* rv = reinterpret_cast<uint16_t*>(img + L.rv);
+    for (int i = tid; i < n_res * D; i += blockDim.x) {
+      const int t = i / D, ch = i % D, slot = (res_start + t) & (SLOTS - 1);
+      const float kf = __uint_as_float((uint32_t)c.kres[((size_t)unit * SLOTS + slot) * D + ch] << 16);
+      const float vf = __uint_as_float((uint32_t)c.vres[((size_t)unit * D + ch) * SLOTS + slot] << 16);
+      rk[i] = __half_as_ushort(__float2half_rn(kf));
+      rv[i] = __half_as_ushort(__float2half_rn(vf));
+    }
+  } else if (rank) {
+    uint16_t* S = reinterpret_cast<uint16_t*>(img + L.S);
+    uint16_t* P = reinterpret_cast<uint16_t*>(img + L.P);
+    for (int i = (bx - n - 1) * blockDim.x + tid; i < D * RANK + RANK; i += (gridDim.x - n - 1) * blockDim.x) {
+      if (i < D * RANK) S[i] = __half_as_ushort(__float2half_rn(c.S[(size_t)unit * D * RANK + i]));
+      else P[i - D * RANK] = __half_as_ushort(__float2half_rn(c.P[(size_t)unit * RANK + i - D * RANK]));
+    }
+  }
+}
+
+// deserialize_cache (cache.py:252-307) into the device layouts: reference words ->
+// dense code tile in shared memory -> pack_k_word / pack_v_word; residual loaded at
+// ring slot 0 (f16 -> bf16, the serving cache's residual precision); S / P from f16
+// (zero when rank = 0); the sequence counters of unit / Hkv.
+__global__ void deserialize_unit_kernel(kvlc_cache c, int unit, int n, int n_res, int rank,
+                                        const uint8_t* __restrict__ img) {
+  const ImageLayout L(n, n_res, rank);
+  const int bx = blockIdx.x, tid = threadIdx.x;
+  if (bx < n) {
+    __shared__ uint8_t codes[G * D];
+    const size_t cb = (size_t)unit * c.max_chunks + bx;
+    const uint32_t* kw = reinterpret_cast<const uint32_t*>(img + L.kcodes) + (size_t)bx * 1024;
+    const uint32_t* vw = reinterpret_cast<const uint32_t*>(img + L.vcodes) + (size_t)bx * G * 8;
+    for (int i = tid; i < G * D; i += blockDim.x) {
+      const int t = i / D, ch = i % D;
+      codes[i] = (uint8_t)((kw[(t >> 4) * 128 + ch] >> (2 * (t & 15))) & 3u);
+    }
+    __syncthreads();
+    for (int wi = tid; wi < 1024; wi += blockDim.x) c.kcodes[cb * 1024 + wi] = pack_k_word(codes, wi);
+    __syncthreads();
+    for (int i = tid; i < G * D; i += blockDim.x) {
+      const int t = i / D, ch = i % D;
+      codes[i] = (uint8_t)((vw[t * 8 + (ch >> 4)] >> (2 * (ch & 15))) & 3u);
+    }
+    __syncthreads();
+    for (int wi = tid; wi < 1024; wi += blockDim.x) c.vcodes[cb * 1024 + wi] = pack_v_word(codes, wi);
+    const uint16_t* km = reinterpret_cast<const uint16_t*>(img + L.kmeta) + (size_t)bx * 2 * D;
+    const uint16_t* vs = reinterpret_cast<const uint16_t*>(img + L.vscale) + (size_t)bx * G;
+    const uint16_t* vz = reinterpret_cast<const uint16_t*>(img + L.vzero) + (size_t)bx * G;
+    for (int i = tid; i < 128; i += blockDim.x) {
+      c.kscale[cb * D + i] = km[i];
+      c.kzero[cb * D + i] = km[D + i];
+      c.vscale[cb * G + i] = vs[i];
+      c.vzero[cb * G + i] = vz[i];
+    }
+  } else if (bx == n) {
+    const uint16_t* rk = reinterpret_cast<const uint16_t*>(img + L.rk);
+    const uint16_t* rv = reinterpret_cast<const uint16_t*>(img + L.rv);
+    for (int i = tid; i < n_res * D; i += blockDim.x) {
+      const int t = i / D, ch = i % D;
+      c.kres[((size_t)unit * SLOTS + t) * D + ch] = __bfloat16_as_ushort(__float2bfloat16_rn(__half2float(__ushort_as_half(rk[i]))));
+      c.vres[((size_t)unit * D + ch) * SLOTS + t] = __bfloat16_as_ushort(__float2bfloat16_rn(__half2float(__ushort_as_half(rv[i]))));
+    }
+    if (tid == 0) {
+      const int b = unit / c.Hkv;
+      c.n_chunks[b] = n;
+      c.res_start[b] = 0;
+      c.res_len[b] = n_res;
+    }
+  } else {
+    const uint16_t* S = reinterpret_cast<const uint16_t*>(img + L.S);
+    const uint16_t* P = reinterpret_cast<const uint16_t*>(img + L.P);
+    for (int i = (bx - n - 1) * blockDim.x + tid; i < D * RANK + RANK; i += (gridDim.x - n - 1) * blockDim.x) {
+      if (i < D * RANK) c.S[(size_t)unit * D * RANK + i] = rank ? __half2float(__ushort_as_half(S[i])) : 0.f;
+      else c.P[(size_t)unit * RANK + i - D * RANK] = rank ? __half2float(__ushort_as_half(P[i - D * RANK])) : 0.f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Prefill flush with the adapter-state update on the 5th-generation tensor
 // cores (tcgen05).  One CTA per (unit, feature half h, chunk range): W_h (the
 // 128 features of W1k or W2k, fp16 hi + lo) stays resident in shared memory;
@@ -1278,6 +1415,41 @@ int kvlc_append(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k_t
   }
   append_finalize_kernel<<<1, 256, 0, s>>>(*c, seq);
   return check_launch("append_finalize");
+}
+
+size_t kvlc_unit_image_bytes(int32_t n_chunks, int32_t res_len, int32_t rank) {
+  if (n_chunks < 0 || res_len < 0 || res_len > SLOTS || !(rank == 0 || rank == RANK)) return 0;
+  return ImageLayout(n_chunks, res_len, rank).end;
+}
+
+int kvlc_serialize_unit(const kvlc_cache* c, int32_t unit, int32_t n_chunks, int32_t res_start, int32_t res_len,
+                        int32_t rank, uint8_t* image, void* stream) {
+  KVLC_NEED_DEVICE();
+  int rc = check_cache(c);
+  if (rc) return rc;
+  KVLC_REQUIRE(unit >= 0 && unit < c->B * c->Hkv, "unit %d out of range", unit);
+  KVLC_REQUIRE(n_chunks >= 0 && n_chunks <= c->max_chunks, "%d chunks exceeds capacity of %d chunks", n_chunks,
+               c->max_chunks);
+  KVLC_REQUIRE(res_len >= 0 && res_len <= SLOTS && res_start >= 0 && res_start < SLOTS, "residual range (%d, %d)",
+               res_start, res_len);
+  KVLC_REQUIRE(rank == 0 || rank == RANK, "cache state rank %d (serving cache holds %d)", rank, RANK);
+  serialize_unit_kernel<<<n_chunks + 1 + (rank ? 32 : 0), 256, 0, as_stream(stream)>>>(*c, unit, n_chunks, res_start,
+                                                                                          res_len, rank, image);
+  return check_launch("serialize_unit");
+}
+
+int kvlc_deserialize_unit(const kvlc_cache* c, int32_t unit, const uint8_t* image, int32_t n_chunks,
+                          int32_t res_len, int32_t rank, void* stream) {
+  KVLC_NEED_DEVICE();
+  int rc = check_cache(c);
+  if (rc) return rc;
+  KVLC_REQUIRE(unit >= 0 && unit < c->B * c->Hkv, "unit %d out of range", unit);
+  KVLC_REQUIRE(n_chunks >= 0 && n_chunks <= c->max_chunks, "cache of %d chunks exceeds capacity of %d chunks",
+               n_chunks, c->max_chunks);
+  KVLC_REQUIRE(res_len >= 0 && res_len <= SLOTS, "residual length %d exceeds the ring (%d)", res_len, SLOTS);
+  KVLC_REQUIRE(rank == 0 || rank == RANK, "cache state rank %d (serving cache holds %d)", rank, RANK);
+  deserialize_unit_kernel<<<n_chunks + 1 + 32, 256, 0, as_stream(stream)>>>(*c, unit, n_chunks, res_len, rank, image);
+  return check_launch("deserialize_unit");
 }
 
 int kvlc_export_chunk(const kvlc_cache* c, int32_t unit, int32_t chunk, uint32_t* kwords,

@@ -118,3 +118,30 @@ def test_oracle_gqa_wrapper_shapes():
                                group=32, window=32)]]
     out = orc.decode_gqa(g.standard_normal((1, 2, 16)), caches, None)
     assert out.shape == (1, 2, 16) and np.all(np.isfinite(out))
+
+
+def test_kvlc_format_round_trips_reference_bytes(golden):
+    """Host side of the .kvlc format (paper_2510_05373_b200/kvlc_format.py): the
+    parsed sections re-join to the reference's bytes; the reader's errors carry
+    the reference's messages (cache.py:233-304)."""
+    import pytest
+    from paper_2510_05373_b200 import kvlc_format as fmt
+    z = golden["cache"]
+    names = sorted({k.split("/")[0] for k in z if k.endswith("/kvlc")})
+    assert "c_prod" in names
+    for name in names:
+        ref = z[f"{name}/kvlc"].tobytes()
+        h = fmt.parse_header(ref)
+        assert h.nbytes() == len(ref)
+        assert fmt.join(h, fmt.split(ref, h)) == ref, name
+    ref = z["c_prod/kvlc"].tobytes()
+    with pytest.raises(fmt.CacheFormatError, match="bad magic at byte 0"):
+        fmt.parse_header(b"XXXX" + ref[4:])
+    with pytest.raises(fmt.CacheFormatError, match="unsupported cache version 2 at byte 4"):
+        fmt.parse_header(ref[:4] + (2).to_bytes(4, "little") + ref[8:])
+    h = fmt.parse_header(ref)
+    with pytest.raises(fmt.CacheFormatError, match="truncated cache file at byte"):
+        fmt.split(ref[:-1], h)
+    with pytest.raises(fmt.CacheFormatError, match="trailing bytes at byte"):
+        fmt.split(ref + b"\0", h)
+    assert issubclass(fmt.CacheFormatError, ValueError)

@@ -146,3 +146,14 @@ def test_value_rotation_tie_is_reference_ordered(seed):
     assert np.array_equal(orc.rotate_post(blk), ref)
     codes, s, zz = orc.quantize_rows(orc.rotate_post(blk), 2, 128)
     assert codes[39, 17] == 1
+
+
+def test_serialization_matches_reference(golden):
+    """.kvlc bytes (cache.py:197-307): the oracle writer reproduces the reference's
+    serialize_cache output byte for byte; the reader round-trips it."""
+    z, names = _cache_cases(golden)
+    for name in names:
+        c, _ = _build(z, name)
+        ref = z[f"{name}/kvlc"].tobytes()
+        assert orc.serialize(c) == ref, name
+        assert orc.serialize(orc.deserialize(ref)) == ref, name
