@@ -7,9 +7,10 @@
 // e^{-M}-consistent rule (_reduce_blocks, attention.py:158-194), the inverse
 // Hadamard rotation of the quantized numerator and the final divide.
 //
-// Kernels (one decode step = 2 launches, PDL-chained):
-//   phi_kernel      phi_q(q) per q-head and C_d = P . phi      (attention.py:224-228)
+// Kernels (one decode step = 1 launch):
 //   split_kernel    per CTA task, selected by blockIdx:
+//                   * correction (first, one per unit): phi_q of the unit's
+//                     query heads, C_d = P phi, C_n = S phi (attention.py:224-231)
 //                   * quantized split: chunks of one (b, kv-head) unit, GQA
 //                     heads batched on the MMA N dimension, 2-bit codes turned
 //                     into fp16 MMA operands by one LOP3 each (exact subnormal
@@ -17,7 +18,6 @@
 //                     (hi+lo fp16 split when the group has <= 4 heads)
 //                     (kvlc_quant.cuh)
 //                   * residual half: bf16 ring window, masked
-//                   * correction rows: C_n = S phi for 32 rows of S
 //                   the last CTA of each unit performs the LSE merge of the
 //                   unit's records + correction, the warp FWHT (H^T = H) and
 //                   the divide (no separate combine launch).
@@ -44,8 +44,6 @@ constexpr int REC = 4 + D;  // record: m (log2 units), l, pad, pad, y[D] (16-byt
 constexpr int PREC = 4 + 2 * D;  // device-partial record: m, l, pad, pad, y_rot[D], y_raw[D]
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float C0 = 0.12751743074173226f;  // log2(e) / sqrt(128)
-constexpr int CORR_ROWS = 32;               // S rows per correction CTA
-constexpr int CORR_CTAS = D / CORR_ROWS;
 
 __device__ __forceinline__ float bf2f(uint16_t x) { return __uint_as_float((uint32_t)x << 16); }
 
@@ -104,7 +102,8 @@ __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.
 struct DecArgs {
   kvlc_cache c;
   const uint16_t* q;      // [B][Hq][D] bf16
-  const float* phi;       // [B][Hq][RANK]
+  const float* w1q;       // [Hkv][D][HALF] fp32 (phi_q weights, adapter.py:91-93)
+  const float* w2q;
   float* corr;            // [B][Hq][1 + D]  (C_d, C_n)
   float* rec;             // [U][nrec][NG][REC]
   int nsq;                // quantized split CTAs per unit
@@ -120,90 +119,6 @@ struct DecArgs {
   void* out;              // [B][Hq][D] bf16 / f32 (final output)
   float* rec_out;         // partial mode: [B][Hq][PREC] (split-KV across devices)
 };
-
-// ---------------------------------------------------------------- phi_q ----
-// One CTA per (kv head, block of PHI_QB queries of that kv head): the queries
-// of all sequences that share W1q/W2q are batched, so each W column is read
-// once per block (coalesced across the 256 feature threads).
-constexpr int PHI_QB = 8;
-
-__global__ void __launch_bounds__(256) phi_kernel(kvlc_cache c, int NG, const float* __restrict__ w1q,
-                                                  const float* __restrict__ w2q,
-                                                  const uint16_t* __restrict__ q,
-                                                  float* __restrict__ phi, float* __restrict__ corr) {
-  griddep_launch();
-  __shared__ float qs[PHI_QB][D];
-  __shared__ float red[8][PHI_QB];
-  __shared__ float stat[2][PHI_QB];
-  const int kvh = blockIdx.x, j0 = blockIdx.y * PHI_QB, nj = c.B * NG;
-  const int f = threadIdx.x, warp = f >> 5, lane = f & 31, half = f >> 7;
-  // query j of this kv head = (b = j / NG, head kvh*NG + j % NG)
-  auto qrow = [&](int j) { return (size_t)(j / NG) * c.Hq + (size_t)kvh * NG + j % NG; };
-  for (int i = f; i < PHI_QB * D; i += 256) {
-    const int j = j0 + i / D;
-    qs[i / D][i % D] = j < nj ? bf2f(q[qrow(j) * D + i % D]) : 0.f;
-  }
-  __syncthreads();
-  const float* W = (half ? w2q : w1q) + (size_t)kvh * D * HALF + (f & (HALF - 1));
-  float acc[PHI_QB];
-#pragma unroll
-  for (int i = 0; i < PHI_QB; ++i) acc[i] = 0.f;
-#pragma unroll 8
-  for (int ch = 0; ch < D; ++ch) {
-    const float w = __ldg(W + ch * HALF);
-#pragma unroll
-    for (int i = 0; i < PHI_QB; ++i) acc[i] = fmaf(qs[i][ch], w, acc[i]);
-  }
-  // max-shifted softmax within each half (linalg.py:38-47)
-#pragma unroll
-  for (int i = 0; i < PHI_QB; ++i) {
-    const float m = warp_max(acc[i]);
-    if (lane == 0) red[warp][i] = m;
-  }
-  __syncthreads();
-  if (f < 2 * PHI_QB) {
-    const int h = f / PHI_QB, i = f % PHI_QB;
-    stat[h][i] = fmaxf(fmaxf(red[4 * h][i], red[4 * h + 1][i]), fmaxf(red[4 * h + 2][i], red[4 * h + 3][i]));
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < PHI_QB; ++i) acc[i] = expf(acc[i] - stat[half][i]);
-#pragma unroll
-  for (int i = 0; i < PHI_QB; ++i) {
-    const float s = warp_sum(acc[i]);
-    if (lane == 0) red[warp][i] = s;
-  }
-  __syncthreads();
-  if (f < 2 * PHI_QB) {
-    const int h = f / PHI_QB, i = f % PHI_QB;
-    stat[h][i] = (red[4 * h][i] + red[4 * h + 1][i]) + (red[4 * h + 2][i] + red[4 * h + 3][i]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < PHI_QB; ++i) {
-    const int j = j0 + i;
-    const float ph = acc[i] / stat[half][i];
-    float cd = 0.f;
-    if (j < nj) {
-      phi[qrow(j) * RANK + f] = ph;
-      cd = c.P[((size_t)(j / NG) * c.Hkv + kvh) * RANK + f] * ph;
-    }
-    acc[i] = cd;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < PHI_QB; ++i) {
-    const float s = warp_sum(acc[i]);
-    if (lane == 0) red[warp][i] = s;
-  }
-  __syncthreads();
-  if (f < PHI_QB && j0 + f < nj) {
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s += red[w][f];
-    corr[qrow(j0 + f) * (1 + D)] = s;  // C_d = P . phi_q
-  }
-}
 
 #include "kvlc_quant.cuh"
 
@@ -328,66 +243,163 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
   cta_merge<NG>(smrec, a.rec + ((size_t)unit * a.nrec + a.nsq + hf) * NG * REC);
 }
 
-// C_n = S phi for CORR_ROWS rows of S (8 per warp).  Waits for phi_kernel.
+// Correction of one unit (attention.py:224-231): phi_q of the unit's NG query heads
+// (feature_map, adapter.py:80-88: thread t owns feature t of each half, W columns
+// read from L2 8 channels at a time), then C_d = P . phi and C_n = S phi for all
+// 128 rows of S (8 / 4 rows per warp per pass, lanes across the 256 features).  These
+// CTAs come first in the grid, so their S stream overlaps the code stream.
 template <int NG>
-__device__ void run_corr(const DecArgs& a, int unit, int rb) {
-  griddep_wait();
+__device__ void run_corr(const DecArgs& a, int unit, float* smf) {
+  static_assert(HALF == THREADS, "one feature of each half per thread");
   const kvlc_cache& c = a.c;
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const size_t qh0 = (size_t)b * c.Hq + (size_t)kvh * NG;
+  float* qs = smf;                    // [NG][D]
+  float* phs = qs + NG * D;           // [NG][RANK]
+  float* red = phs + NG * RANK;       // [WARPS][2 NG]
+  float* stat = red + WARPS * 2 * NG; // [2 NG]
+  for (int i = t; i < NG * D; i += THREADS) qs[i] = bf2f(a.q[(qh0 + i / D) * D + i % D]);
+  __syncthreads();
+  float z[2][NG];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) z[0][i] = z[1][i] = 0.f;
+  const float* W1 = a.w1q + (size_t)kvh * D * HALF + t;
+  const float* W2 = a.w2q + (size_t)kvh * D * HALF + t;
+#pragma unroll 1
+  for (int c0 = 0; c0 < D; c0 += 8) {
+    float w1[8], w2[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      w1[k] = __ldg(W1 + (size_t)(c0 + k) * HALF);
+      w2[k] = __ldg(W2 + (size_t)(c0 + k) * HALF);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k += 4) {
+#pragma unroll
+      for (int i = 0; i < NG; ++i) {
+        const float4 x = *reinterpret_cast<const float4*>(qs + i * D + c0 + k);
+        z[0][i] = fmaf(x.x, w1[k], z[0][i]);
+        z[0][i] = fmaf(x.y, w1[k + 1], z[0][i]);
+        z[0][i] = fmaf(x.z, w1[k + 2], z[0][i]);
+        z[0][i] = fmaf(x.w, w1[k + 3], z[0][i]);
+        z[1][i] = fmaf(x.x, w2[k], z[1][i]);
+        z[1][i] = fmaf(x.y, w2[k + 1], z[1][i]);
+        z[1][i] = fmaf(x.z, w2[k + 2], z[1][i]);
+        z[1][i] = fmaf(x.w, w2[k + 3], z[1][i]);
+      }
+    }
+  }
+  // max-shifted softmax of each half (linalg.py:38-47)
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      const float m = warp_max(z[h][i]);
+      if (lane == 0) red[warp * 2 * NG + h * NG + i] = m;
+    }
+  __syncthreads();
+  if (t < 2 * NG) {
+    float m = red[t];
+#pragma unroll
+    for (int w = 1; w < WARPS; ++w) m = fmaxf(m, red[w * 2 * NG + t]);
+    stat[t] = m;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < NG; ++i) z[h][i] = expf(z[h][i] - stat[h * NG + i]);
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      const float sm_ = warp_sum(z[h][i]);
+      if (lane == 0) red[warp * 2 * NG + h * NG + i] = sm_;
+    }
+  __syncthreads();
+  if (t < 2 * NG) {
+    float sm_ = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) sm_ += red[w * 2 * NG + t];
+    stat[t] = sm_;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < NG; ++i) phs[i * RANK + h * HALF + t] = z[h][i] / stat[h * NG + i];
+  __syncthreads();
+
   float ph[NG][8];
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    const float4* p = reinterpret_cast<const float4*>(a.phi + (qh0 + i) * RANK + lane * 8);
-    float4 x = p[0], y = p[1];
+    const float4 x = *reinterpret_cast<const float4*>(phs + i * RANK + lane * 8);
+    const float4 y = *reinterpret_cast<const float4*>(phs + i * RANK + lane * 8 + 4);
     ph[i][0] = x.x; ph[i][1] = x.y; ph[i][2] = x.z; ph[i][3] = x.w;
     ph[i][4] = y.x; ph[i][5] = y.y; ph[i][6] = y.z; ph[i][7] = y.w;
   }
-  const int row0 = rb * CORR_ROWS + warp * (CORR_ROWS / WARPS);
-  float4 sr[CORR_ROWS / WARPS][2];
-#pragma unroll
-  for (int r = 0; r < CORR_ROWS / WARPS; ++r) {
-    const float4* sp = reinterpret_cast<const float4*>(c.S + ((size_t)unit * D + row0 + r) * RANK + lane * 8);
-    sr[r][0] = __ldg(sp);
-    sr[r][1] = __ldg(sp + 1);
-  }
-  // per-lane partial dots for the warp's 8 rows x NG heads, then one
-  // reduce-scatter per 32 values: lane L ends with the total of value L
-  constexpr int NV = (CORR_ROWS / WARPS) * NG;
-  constexpr int NB = (NV + 31) / 32;
-  float vals[NB * 32];
-#pragma unroll
-  for (int n = 0; n < NB * 32; ++n) vals[n] = 0.f;
-#pragma unroll
-  for (int r = 0; r < CORR_ROWS / WARPS; ++r) {
-    const float s8[8] = {sr[r][0].x, sr[r][0].y, sr[r][0].z, sr[r][0].w,
-                         sr[r][1].x, sr[r][1].y, sr[r][1].z, sr[r][1].w};
+  if (warp == 0) {  // C_d = P . phi_q (attention.py:228)
+    const float4* pp = reinterpret_cast<const float4*>(c.P + (size_t)unit * RANK + lane * 8);
+    const float4 x = __ldg(pp), y = __ldg(pp + 1);
+    const float p8[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
       float v = 0.f;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v = fmaf(s8[k], ph[i][k], v);
-      vals[r * NG + i] = v;
+      for (int k = 0; k < 8; ++k) v = fmaf(p8[k], ph[i][k], v);
+      v = warp_sum(v);
+      if (lane == 0) a.corr[(qh0 + i) * (1 + D)] = v;
     }
   }
+  // C_n = S phi (attention.py:227): per pass a warp takes RPW rows; per-lane partial
+  // dots, then one reduce-scatter per 32 values (lane L ends with value L's total)
+  constexpr int RPW = NG > 4 ? 4 : 8;  // rows per warp per pass (register budget at 8 heads)
+  constexpr int NV = RPW * NG;
+  constexpr int NB = (NV + 31) / 32;
+#pragma unroll 1
+  for (int row0 = warp * RPW; row0 < D; row0 += WARPS * RPW) {
+    float4 sr[RPW][2];
 #pragma unroll
-  for (int blk = 0; blk < NB; ++blk) {
-    float* x = vals + 32 * blk;
+    for (int r = 0; r < RPW; ++r) {
+      const float4* sp = reinterpret_cast<const float4*>(c.S + ((size_t)unit * D + row0 + r) * RANK + lane * 8);
+      sr[r][0] = __ldg(sp);
+      sr[r][1] = __ldg(sp + 1);
+    }
+    float vals[NB * 32];
 #pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-      const bool upper = lane & s;
+    for (int n = 0; n < NB * 32; ++n) vals[n] = 0.f;
 #pragma unroll
-      for (int k = 0; k < s; ++k) {
-        const float send = upper ? x[k] : x[k + s];
-        const float keep = upper ? x[k + s] : x[k];
-        x[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    for (int r = 0; r < RPW; ++r) {
+      const float s8[8] = {sr[r][0].x, sr[r][0].y, sr[r][0].z, sr[r][0].w,
+                           sr[r][1].x, sr[r][1].y, sr[r][1].z, sr[r][1].w};
+#pragma unroll
+      for (int i = 0; i < NG; ++i) {
+        float v = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v = fmaf(s8[k], ph[i][k], v);
+        vals[r * NG + i] = v;
       }
     }
-    const int n = 32 * blk + lane;
-    if (n < NV) {
-      const int r = n / NG, i = n % NG;
-      a.corr[(qh0 + i) * (1 + D) + 1 + row0 + r] = x[0];
+#pragma unroll
+    for (int blk = 0; blk < NB; ++blk) {
+      float* x = vals + 32 * blk;
+#pragma unroll
+      for (int sft = 16; sft >= 1; sft >>= 1) {
+        const bool upper = lane & sft;
+#pragma unroll
+        for (int k = 0; k < sft; ++k) {
+          const float send = upper ? x[k] : x[k + sft];
+          const float keep = upper ? x[k + sft] : x[k];
+          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
+      }
+      const int n = 32 * blk + lane;
+      if (n < NV) {
+        const int r = n / NG, i = n % NG;
+        a.corr[(qh0 + i) * (1 + D) + 1 + row0 + r] = x[0];
+      }
     }
   }
 }
@@ -553,22 +565,20 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   __shared__ __align__(16) SplitSmem sm;
   __shared__ int last;
   const int U = a.c.B * a.c.Hkv;
+  const int ncorr = a.tail && a.corr_on ? U : 0;  // correction CTAs first (their S stream overlaps)
   int x = blockIdx.x, unit;
-  if (x < U * a.nsq) {
+  if (x < ncorr) {
+    unit = x;
+    run_corr<NG>(a, unit, sm.rec);
+  } else if ((x -= ncorr) < U * a.nsq) {
     unit = x / a.nsq;
     run_quant<NG, EXTRA>(a, unit, x % a.nsq, sm);
   } else {
     x -= U * a.nsq;
-    if (x < 2 * U) {
-      unit = x / 2;
-      run_resid<NG>(a, unit, x % 2, sm.rec);
-    } else {
-      x -= 2 * U;
-      unit = x / CORR_CTAS;
-      run_corr<NG>(a, unit, x % CORR_CTAS);
-    }
+    unit = x / 2;
+    run_resid<NG>(a, unit, x % 2, sm.rec);
   }
-  const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? CORR_CTAS : 0) : 0);
+  const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? 1 : 0) : 0);
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();  // publish this CTA's record / correction rows
@@ -577,7 +587,6 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (a.corr_on) griddep_wait();  // C_d comes from phi_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = unit / a.c.Hkv, kvh = unit % a.c.Hkv;
   for (int h = warp; h < NG; h += WARPS) combine_head(a, NG, b, h, kvh, lane);
@@ -626,7 +635,7 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
 // ------------------------------------------------------------- host ----
 struct Plan {
   int NG, U, nsq, cpc, nrec, corr_on;
-  size_t done_off, phi_off, corr_off, rec_off, total;
+  size_t done_off, corr_off, rec_off, total;
 };
 
 int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int chunk_hi, int tail,
@@ -650,14 +659,12 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   p.corr_on = corr_on && tail ? 1 : 0;
   p.nrec = p.nsq + (tail ? 2 : 0);
   size_t BH = (size_t)c->B * c->Hq;
-  p.phi_off = 0;
-  p.corr_off = align_up(BH * RANK * sizeof(float));
-  p.rec_off = p.corr_off + align_up(BH * (1 + D) * sizeof(float));
+  p.corr_off = 0;
+  p.rec_off = align_up(BH * (1 + D) * sizeof(float));
   // arrival counters first: their offset must not depend on the split plan
   // (they are zero-initialised once and left at zero by every launch)
   p.done_off = 0;
   const size_t base = align_up((size_t)p.U * sizeof(uint32_t));
-  p.phi_off += base;
   p.corr_off += base;
   p.rec_off += base;
   p.total = p.rec_off + align_up((size_t)p.U * p.nrec * p.NG * REC * sizeof(float));
@@ -668,19 +675,15 @@ template <int NG>
 int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, const Plan& p,
               char* ws, int chunk_lo, int chunk_hi, int tail, float* corr_ext, int literal,
               int out_fp32, void* out, float* rec_out, const kvlc_decode_opts* o, cudaStream_t s) {
-  float* phi = reinterpret_cast<float*>(ws + p.phi_off);
   float* corr = corr_ext ? corr_ext : reinterpret_cast<float*>(ws + p.corr_off);
   float* rec = reinterpret_cast<float*>(ws + p.rec_off);
-  if (p.corr_on) {
-    phi_kernel<<<dim3(c->Hkv, (c->B * NG + PHI_QB - 1) / PHI_QB), 256, 0, s>>>(*c, NG, ad->w1q, ad->w2q, q,
-                                                                             phi, corr);
-    int rc = check_launch("phi");
-    if (rc) return rc;
-  }
   DecArgs a{};
   a.c = *c;
   a.q = q;
-  a.phi = phi;
+  if (p.corr_on) {
+    a.w1q = ad->w1q;
+    a.w2q = ad->w2q;
+  }
   a.corr = corr;
   a.rec = rec;
   a.nsq = p.nsq;
@@ -695,20 +698,12 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   a.out_fp32 = out_fp32;
   a.out = out;
   a.rec_out = rec_out;
-  int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? p.U * CORR_CTAS : 0) : 0);
+  int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? p.U : 0) : 0);
   cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
   cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = p.corr_on ? 1 : 0;
-  if (o && o->ev_begin) {
-    KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_begin), s));
-    cfg.numAttrs = 0;  // the event already orders the launch
-  }
+  if (o && o->ev_begin) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_begin), s));
   if (NG <= 4) {
     KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a));
   } else {
