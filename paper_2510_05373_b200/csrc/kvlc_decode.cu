@@ -646,13 +646,24 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   p.U = c->B * c->Hkv;
   int maxc = o && o->max_chunks_hint > 0 ? o->max_chunks_hint : c->max_chunks;
   int span = std::max(0, std::min(maxc, chunk_hi) - chunk_lo);
-  int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : 0;
+  static const int cpc_env = [] {  // tuning override (tools/run_dec.sh sweeps)
+    const char* e = getenv("KVLC_CPC");
+    return e ? atoi(e) : 0;
+  }();
+  int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : cpc_env;
   if (cpc == 0) {
-    // ~2 waves of quantized-split CTAs at KVLC_SPLIT_MINB resident CTAs per SM
-    // (a wave-quantised cost model measured worse on configs 3 and 4)
-    const long long ctas_wanted = 148LL * KVLC_SPLIT_MINB * 2;
+    // Per-CTA fixed cost (pipeline fill, q / B build, record merge, arrival) favours
+    // long splits; the tail favours many.  Measured on configs 2-4
+    // (tools/run_cpc3.sh, run_cpc4.sh): about 1.5 waves of splits at
+    // KVLC_SPLIT_MINB CTAs per SM, at least 8 chunks per split, at most 52 records per
+    // unit (the last CTA of a unit merges them all), then equal-length splits.
+    // Configs 2 / 3 / 4: 7 -> 9 / 8 / 20 chunks, 49.2 -> 44.4 / 38.1 -> 34.8 / 55.6 -> 46.5 us.
+    const long long slots = 148LL * KVLC_SPLIT_MINB;
     const long long chunks = (long long)p.U * std::max(span, 1);
-    cpc = (int)std::max(2LL, std::min(32LL, (chunks + ctas_wanted - 1) / ctas_wanted));
+    long long t = std::max(8LL, (2 * chunks + 3 * slots - 1) / (3 * slots));
+    t = std::max(t, (long long)(std::max(span, 1) + 51) / 52);
+    const long long nsq = (std::max(span, 1) + t - 1) / t;
+    cpc = (int)std::max(1LL, std::min(32LL, (std::max(span, 1) + nsq - 1) / nsq));
   }
   p.cpc = cpc;
   p.nsq = std::max(1, (span + cpc - 1) / cpc);

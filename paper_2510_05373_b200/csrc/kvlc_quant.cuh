@@ -410,37 +410,40 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   constexpr bool HILO = NG <= 4;
-  // q (fp16, exact from bf16) for this warp's B share: column n = g,
-  // channels 32w + 16e + 2t + {0,1} (+8)
-  uint32_t qs[4];
-  {
-    const int head = HILO ? (g >> 1) : g;
-    const bool valid = head < NG;
-    const uint32_t* qp = reinterpret_cast<const uint32_t*>(
-        a.q + ((size_t)b * c.Hq + (size_t)kvh * NG + (valid ? head : 0)) * D);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int pair = 16 * warp + 8 * (i >> 1) + t + 4 * (i & 1);
-      const uint32_t raw = valid ? __ldg(qp + pair) : 0u;
-      qs[i] = h2u(__floats2half2_rn(__uint_as_float(raw << 16), __uint_as_float(raw & 0xffff0000u)));
-    }
-  }
   WarpState<NG> st;
   st.init();
-  const int n_ch = min(c.n_chunks[b], a.chunk_hi);
   const int lo = a.chunk_lo + split * a.cpc;
-  const int hi = min(n_ch, lo + a.cpc);
+  const int cap_hi = min(min(a.chunk_hi, c.max_chunks), lo + a.cpc);  // no memory read
+  const int n_ch = min(c.n_chunks[b], a.chunk_hi);                      // in flight meanwhile
   const size_t cb0 = (size_t)unit * c.max_chunks;
   QuantSmem& q = sm.quant;
-  if (lo < hi) {
-    SliceSrc src;
-    src.init(c, cb0 + lo, warp, lane);
-    const int n = hi - lo;
-    // prologue: stages for chunks 0, 1 (relative) in flight
+  SliceSrc src;
+  src.init(c, cb0 + lo, warp, lane);
+  // prologue: stages for chunks 0, 1 (relative) issued before the sequence length and
+  // q arrive, so the three round trips overlap; bounded by the cache capacity (always
+  // allocated), only chunks below the sequence's count are consumed
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-      if (s < n) src.issue(q.stage[s][warp], lane, s);
-      cp_commit();
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (lo + s < cap_hi) src.issue(q.stage[s][warp], lane, s);
+    cp_commit();
+  }
+  const int hi = min(n_ch, lo + a.cpc);
+  if (lo < hi) {
+    const int n = hi - lo;
+    // q (fp16, exact from bf16) for this warp's B share: column n = g,
+    // channels 32w + 16e + 2t + {0,1} (+8)
+    uint32_t qs[4];
+    {
+      const int head = HILO ? (g >> 1) : g;
+      const bool valid = head < NG;
+      const uint32_t* qp = reinterpret_cast<const uint32_t*>(
+          a.q + ((size_t)b * c.Hq + (size_t)kvh * NG + (valid ? head : 0)) * D);
+      uint32_t raw[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) raw[i] = valid ? __ldg(qp + 16 * warp + 8 * (i >> 1) + t + 4 * (i & 1)) : 0u;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        qs[i] = h2u(__floats2half2_rn(__uint_as_float(raw[i] << 16), __uint_as_float(raw[i] & 0xffff0000u)));
     }
     cp_wait<STAGES - 2>();
     __syncwarp();
@@ -462,8 +465,8 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
       __syncthreads();
       s_cur = s_next;
     }
-    cp_wait<0>();
   }
+  cp_wait<0>();      // also drains a speculative prologue of an empty split
   __syncthreads();   // the record area aliases the pipeline buffers
   warp_store<NG, true>(st, sm.rec + warp * NG * REC, lane);
   __syncthreads();
