@@ -160,14 +160,16 @@ def test_split_partials_merge_equals_full_decode():
             if tail:
                 corr = c
         merged = merge_records(torch.stack(recs), corr, out_dtype=F32)
-        # different split boundaries only change fp32 summation order
+        # different split boundaries change the fp32 summation order and each split's
+        # lazy-rescale reference point, relative to which p * s_v becomes an fp16 hi / lo
+        # MMA operand: ~1e-4 of max|out|, inside T4's 1e-3 (the oracle checks above)
         e = (merged - full).abs().max().item() / full.abs().max().item()
-        assert e <= 5e-5, f"parts={parts} rel diff {e:.3e}"
+        assert e <= 2e-4, f"parts={parts} rel diff {e:.3e}"
         for literal in (True,):
             m2 = merge_records(torch.stack(recs), corr, literal=literal, out_dtype=F32)
             f2 = cache.decode(qd, adapters=bank, literal=literal, out_dtype=F32)
             e = (m2 - f2).abs().max().item() / f2.abs().max().item()
-            assert e <= 5e-5, f"literal parts={parts} rel diff {e:.3e}"
+            assert e <= 2e-4, f"literal parts={parts} rel diff {e:.3e}"
 
 
 def test_correction_dominated_extremes():
