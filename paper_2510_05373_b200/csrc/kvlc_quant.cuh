@@ -6,8 +6,10 @@
 //     slice's V scale/zero and the K scale/zero of its B-operand share)
 //     through a 3-stage cp.async pipeline in shared memory;
 //   * the QK^T B operand of a chunk (q' = q * s_k, fp16 hi/lo) and the zero
-//     term zt = q . z_k are built cooperatively (warp w: k-tiles 2w, 2w+1),
-//     double-buffered in shared memory, one CTA barrier per chunk;
+//     term zt = q . z_k are built cooperatively (warp w: k-tiles 2w, 2w+1) into
+//     shared buffers guarded by full / empty mbarriers (4 warp arrivals each):
+//     a warp waits only for the B shares it is about to read, not at a CTA
+//     barrier per chunk (43.7 vs 45.1 us on config 2);
 //   * codes become fp16 MMA operands with one LOP3 per register (exact
 //     subnormals c * 4^j * 2^-24 from the fragment-native layouts written by
 //     kvlc_flush.cu); mma.sync m16n8k16, GQA heads on N;
@@ -21,6 +23,10 @@
 #endif
 constexpr int STAGES = KVLC_STAGES;
 constexpr float LAZY = 8.f;
+#ifndef KVLC_BBUF
+#define KVLC_BBUF 2
+#endif
+constexpr int NBUF = KVLC_BBUF;   // B-operand buffers (3 / 4 measured equal: tools/run_dec.sh)
 
 template <int NG>
 struct WarpState {
@@ -77,10 +83,38 @@ struct WarpStage {
 
 struct QuantSmem {
   WarpStage stage[STAGES][WARPS];
-  uint4 bq[2][4][32];   // [buf][k-tile pair][lane]: (b0, b1 of kt = 2p, b0, b1 of kt = 2p+1)
-  uint4 bl[2][4][32];   // low parts (groups of > 4 heads)
-  float4 zt[2][8];      // [buf][column g] -> partial zero terms of the 4 warps
+  uint4 bq[NBUF][4][32];   // [buf][k-tile pair][lane]: (b0, b1 of kt = 2p, b0, b1 of kt = 2p+1)
+  uint4 bl[NBUF][4][32];   // low parts (groups of > 4 heads)
+  float4 zt[NBUF][8];      // [buf][column g] -> partial zero terms of the 4 warps
+  uint64_t full[NBUF];     // 4 warp arrivals: every share of the buffer's B is written
+  uint64_t empty[NBUF];    // 4 warp arrivals: every warp is done reading the buffer
 };
+
+// CTA-scope mbarriers between the 4 warps of a quantized split (one elected lane per
+// warp arrives after __syncwarp, so the whole warp's shared-memory writes are released).
+__device__ __forceinline__ void qb_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+               "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void qb_arrive(uint64_t* bar, int lane) {
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void qb_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
 
 union SplitSmem {
   QuantSmem quant;
@@ -417,6 +451,8 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
   const int n_ch = min(c.n_chunks[b], a.chunk_hi);                      // in flight meanwhile
   const size_t cb0 = (size_t)unit * c.max_chunks;
   QuantSmem& q = sm.quant;
+  if (threadIdx.x < 2 * NBUF) qb_init(threadIdx.x < NBUF ? &q.full[threadIdx.x] : &q.empty[threadIdx.x - NBUF], WARPS);
+  __syncthreads();  // barriers initialised before any warp arrives
   SliceSrc src;
   src.init(c, cb0 + lo, warp, lane);
   // prologue: stages for chunks 0, 1 (relative) issued before the sequence length and
@@ -448,21 +484,25 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
     cp_wait<STAGES - 2>();
     __syncwarp();
     build_b<NG>(q, 0, q.stage[0][warp], qs, warp, lane);
-    __syncthreads();
+    qb_arrive(&q.full[0], lane);
     int s_cur = 0;
     for (int k = 0; k < n; ++k) {
-      const int buf = k & 1;
+      const int buf = k % NBUF;
       const int s_next = s_cur == STAGES - 1 ? 0 : s_cur + 1;
-      const int s_fill = s_cur == 0 ? STAGES - 1 : s_cur - 1;   // freed by chunk k-1
+      const int s_fill = s_cur == 0 ? STAGES - 1 : s_cur - 1;   // freed by chunk k-1 (this warp's own)
       if (k + STAGES - 1 < n) src.issue(q.stage[s_fill][warp], lane, k + STAGES - 1);
       cp_commit();
+      qb_wait(&q.full[buf], (uint32_t)(k / NBUF) & 1u);   // every share of chunk k's B
       quant_chunk<NG, EXTRA>(q.stage[s_cur][warp], q, buf, st, lane);
+      qb_arrive(&q.empty[buf], lane);
       if (k + 1 < n) {
         cp_wait<STAGES - 2>();   // chunk k+1 has landed (only k+2 may be pending)
         __syncwarp();
-        build_b<NG>(q, buf ^ 1, q.stage[s_next][warp], qs, warp, lane);
+        const int nb = (k + 1) % NBUF;
+        if (k + 1 >= NBUF) qb_wait(&q.empty[nb], (uint32_t)((k + 1) / NBUF - 1) & 1u);  // chunk k+1-NBUF done
+        build_b<NG>(q, nb, q.stage[s_next][warp], qs, warp, lane);
+        qb_arrive(&q.full[nb], lane);
       }
-      __syncthreads();
       s_cur = s_next;
     }
   }
