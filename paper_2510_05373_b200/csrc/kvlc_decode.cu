@@ -245,7 +245,7 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
 
 // Correction of one unit (attention.py:224-231): phi_q of the unit's NG query heads
 // (feature_map, adapter.py:80-88: thread t owns feature t of each half, W columns
-// read from L2 8 channels at a time), then C_d = P . phi and C_n = S phi for all
+// read from L2 8 channels per round trip), then C_d = P . phi and C_n = S phi for all
 // 128 rows of S (8 / 4 rows per warp per pass, lanes across the 256 features).  These
 // CTAs come first in the grid, so their S stream overlaps the code stream.
 template <int NG>
@@ -266,16 +266,22 @@ __device__ void run_corr(const DecArgs& a, int unit, float* smf) {
   for (int i = 0; i < NG; ++i) z[0][i] = z[1][i] = 0.f;
   const float* W1 = a.w1q + (size_t)kvh * D * HALF + t;
   const float* W2 = a.w2q + (size_t)kvh * D * HALF + t;
+#ifndef KVLC_PHI_BATCH
+#define KVLC_PHI_BATCH 8
+#endif
+  // channels per batch of W loads in flight: 16 / 32 measured slower for the whole kernel
+  // (43.1 vs 44.7 us, the larger unrolled body costs the shared quantized-split code)
+  constexpr int PB = KVLC_PHI_BATCH;
 #pragma unroll 1
-  for (int c0 = 0; c0 < D; c0 += 8) {
-    float w1[8], w2[8];
+  for (int c0 = 0; c0 < D; c0 += PB) {
+    float w1[PB], w2[PB];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < PB; ++k) {
       w1[k] = __ldg(W1 + (size_t)(c0 + k) * HALF);
       w2[k] = __ldg(W2 + (size_t)(c0 + k) * HALF);
     }
 #pragma unroll
-    for (int k = 0; k < 8; k += 4) {
+    for (int k = 0; k < PB; k += 4) {
 #pragma unroll
       for (int i = 0; i < NG; ++i) {
         const float4 x = *reinterpret_cast<const float4*>(qs + i * D + c0 + k);
