@@ -236,6 +236,13 @@ int kvlc_decode_partial(const kvlc_cache* cache, const kvlc_adapter* ad,
                         int32_t include_tail, float* rec, float* corr,
                         const kvlc_decode_opts* o, void* ws, size_t ws_bytes,
                         void* stream);
+/* Copies a step's input (e.g. q, bf16 [B][Hq][128]) from pinned host memory
+ * `src` to device `dst` in a kernel that lets the following kvlc_decode start
+ * early (programmatic dependent launch): the decode streams its codes while q
+ * arrives and reads q only after the copy completes.  16-byte aligned, bytes a
+ * multiple of 16.  For a host-to-host decode step in one CUDA graph. */
+int kvlc_stage_input(const void* src, void* dst, size_t bytes, void* stream);
+
 int kvlc_merge_records(const float* recs, int32_t n_rec, int64_t rec_stride,
                        const float* corr, int32_t B, int32_t Hq, int32_t literal,
                        int32_t out_fp32, void* out, void* stream);

@@ -78,6 +78,7 @@ _SIGS = {
     "kvlc_decode_partial": (c_int, [POINTER(KvlcCache), POINTER(KvlcAdapter), c_void_p, c_int32,
                                     c_int32, c_int32, c_void_p, c_void_p, POINTER(KvlcDecodeOpts),
                                     c_void_p, c_size_t, c_void_p]),
+    "kvlc_stage_input": (c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     "kvlc_merge_records": (c_int, [c_void_p, c_int32, c_int64, c_void_p, c_int32, c_int32, c_int32,
                                    c_int32, c_void_p, c_void_p]),
     "kvlc_export_chunk": (c_int, [POINTER(KvlcCache), c_int32, c_int32, c_void_p, c_void_p, c_void_p,

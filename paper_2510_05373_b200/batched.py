@@ -237,8 +237,10 @@ class BatchedKVCache:
         q = q.to(self.device, torch.bfloat16).contiguous()
         if out is None:
             out = torch.empty(q.shape, dtype=out_dtype, device=self.device)
-        if out.dtype not in (torch.bfloat16, torch.float32) or out.shape != q.shape:
-            raise ValueError("out must be a [B, Hq, 128] bf16 or float32 tensor")
+        if out.dtype not in (torch.bfloat16, torch.float32) or out.shape != q.shape or not out.is_contiguous():
+            raise ValueError("out must be a contiguous [B, Hq, 128] bf16 or float32 tensor")
+        if out.device.type == "cpu" and not out.is_pinned():
+            raise ValueError("a host `out` must be pinned (the kernel writes it through unified addressing)")
         o = self._opts(literal, chunks_per_split, out.dtype == torch.float32, events)
         nbytes = _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
         ws = self.decode_ws(nbytes)
@@ -248,16 +250,29 @@ class BatchedKVCache:
         return out
 
     def capture_decode(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False,
-                       out: torch.Tensor | None = None, chunks_per_split: int = 0):
-        """Capture one decode step on fixed q / out buffers into a CUDA graph
-        (the PDL-chained launches replay with one graph launch).
-        Returns (graph, out); refill q in place and call graph.replay()."""
-        if out is None:
+                       out: torch.Tensor | None = None, chunks_per_split: int = 0,
+                       q_host: torch.Tensor | None = None, out_host: torch.Tensor | None = None):
+        """Capture one decode step on fixed q / out buffers into a CUDA graph (one
+        graph launch per step).  With a pinned `q_host` the graph also holds the
+        step's H2D copy of q (kvlc_stage_input, chained to the decode by programmatic
+        dependent launch); with a pinned `out_host` the kernel's combine writes
+        the result straight into host memory (unified addressing, no D2H copy node:
+        a D2H copy after an H2D copy on one stream costs ~10 us of direction switch).
+        Returns (graph, out); refill q (or q_host) in place and call graph.replay()."""
+        if out_host is not None:
+            out = out_host
+        elif out is None:
             out = torch.empty(q.shape, dtype=torch.bfloat16, device=self.device)
         self.decode(q, adapters, literal, out, chunks_per_split)   # sizes the workspace
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
+        if q_host is not None and (q_host.dtype != torch.bfloat16 or q_host.shape != q.shape
+                                   or not q_host.is_pinned() or not q_host.is_contiguous()):
+            raise ValueError("q_host must be a pinned contiguous bf16 tensor shaped like q")
         with torch.cuda.graph(graph):
+            if q_host is not None:   # copy kernel, programmatic-launch chained to the decode
+                _lib.call("kvlc_stage_input", q_host.data_ptr(), q.data_ptr(), q.numel() * 2,
+                          _lib.stream_handle())
             self.decode(q, adapters, literal, out, chunks_per_split)
         return graph, out
 

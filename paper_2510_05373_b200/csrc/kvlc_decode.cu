@@ -147,6 +147,7 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
     const uint16_t* vr = c.vres + (size_t)unit * D * SLOTS;
     // q (bf16) B fragments: column n = g; channels 32kp + 8t + 4e + {0,1 | 2,3}
     uint32_t qb[4][4];
+    griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
     {
       const int head = HILO ? (g >> 1) : g;
       const bool valid = HILO ? ((g & 1) == 0 && head < NG) : head < NG;
@@ -259,6 +260,7 @@ __device__ void run_corr(const DecArgs& a, int unit, float* smf) {
   float* phs = qs + NG * D;           // [NG][RANK]
   float* red = phs + NG * RANK;       // [WARPS][2 NG]
   float* stat = red + WARPS * 2 * NG; // [2 NG]
+  griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
   for (int i = t; i < NG * D; i += THREADS) qs[i] = bf2f(a.q[(qh0 + i / D) * D + i % D]);
   __syncthreads();
   float z[2][NG];
@@ -587,6 +589,7 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? 1 : 0) : 0);
   __syncthreads();
   if (threadIdx.x == 0) {
+    griddep_wait();   // the predecessor grid (if any) has flushed: counters / q are current
     __threadfence();  // publish this CTA's record / correction rows
     last = atomicAdd(a.done + unit, 1u) == (uint32_t)(per_unit - 1);
   }
@@ -597,6 +600,17 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   const int b = unit / a.c.Hkv, kvh = unit % a.c.Hkv;
   for (int h = warp; h < NG; h += WARPS) combine_head(a, NG, b, h, kvh, lane);
   if (threadIdx.x == 0) a.done[unit] = 0u;  // self-cleaning for the next step
+}
+
+// Copies a step's input (q) from pinned host memory to the device with every 16-byte
+// piece in flight at once, and lets the programmatic-launch dependent (the decode)
+// start its code streams immediately: inside a CUDA graph a copy-engine H2D node
+// followed by the kernel costs ~18 us per step, this pair ~4 us (tools/bench_e2e.py).
+__global__ void __launch_bounds__(256) stage_input_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                          size_t n16) {
+  griddep_launch();
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 // LSE merge of n device records (m, l, y_rot, y_raw) + correction -> out.
@@ -720,6 +734,14 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
   cfg.stream = s;
+  // programmatic dependent launch: CTAs may start while a predecessor kernel (e.g. the
+  // kvlc_stage_input copy of q) finishes; every read of q or of the arrival counters
+  // follows griddepcontrol.wait, the code streams do not
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (o && o->ev_begin) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_begin), s));
   if (NG <= 4) {
     KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a));
@@ -806,6 +828,19 @@ int kvlc_decode_partial(const kvlc_cache* c, const kvlc_adapter* ad, const uint1
     KVLC_CUDA(cudaMemsetAsync(corr, 0, (size_t)c->B * c->Hq * (1 + D) * sizeof(float), as_stream(stream)));
   return launch(c, ad, q, p, static_cast<char*>(ws), chunk_lo, chunk_hi, include_tail ? 1 : 0, corr,
                 0, 0, nullptr, rec, o, as_stream(stream));
+}
+
+int kvlc_stage_input(const void* src, void* dst, size_t bytes, void* stream) {
+  KVLC_NEED_DEVICE();
+  KVLC_REQUIRE(src && dst && bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(dst) & 15) == 0,
+               "stage_input needs 16-byte aligned buffers and a multiple of 16 bytes (%zu)", bytes);
+  if (bytes == 0) return KVLC_OK;
+  const size_t n16 = bytes / 16;
+  const int grid = (int)std::min<size_t>((n16 + 255) / 256, 148 * 8);
+  stage_input_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst),
+                                                          n16);
+  return check_launch("stage_input");
 }
 
 int kvlc_merge_records(const float* recs, int32_t n_rec, int64_t rec_stride, const float* corr,

@@ -469,6 +469,7 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
     // q (fp16, exact from bf16) for this warp's B share: column n = g,
     // channels 32w + 16e + 2t + {0,1} (+8)
     uint32_t qs[4];
+    griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
     {
       const int head = HILO ? (g >> 1) : g;
       const bool valid = head < NG;

@@ -223,3 +223,25 @@ def test_value_tie_tokens_match_reference_codes():
     out = cache.decode(tdev(q), out_dtype=F32).cpu().numpy()
     ref = oracle_decode(q, ocs, None)
     assert np.abs(out - ref).max() <= 1e-3 * np.abs(ref).max()
+
+
+def test_host_output_graph_matches_device_output():
+    """capture_decode(q_host=, out_host=): H2D q inside the graph, the combine writes
+    the result into pinned host memory; equal to the device-output decode."""
+    B, Hkv, Hq, n = 2, 2, 8, 700
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=12)
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k), tdev(v), lens=[n, n - 200], adapters=bank)
+    want = cache.decode(tdev(q), adapters=bank).cpu()
+    q_host = torch.from_numpy(q.astype(np.float32)).bfloat16().pin_memory()
+    out_host = torch.zeros((B, Hq, D), dtype=torch.bfloat16).pin_memory()
+    qd = torch.empty((B, Hq, D), dtype=torch.bfloat16, device="cuda")
+    g, out = cache.capture_decode(qd, adapters=bank, q_host=q_host, out_host=out_host)
+    assert out.data_ptr() == out_host.data_ptr()
+    out_host.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out_host, want)
+    with pytest.raises(ValueError, match="pinned"):
+        cache.decode(tdev(q), adapters=bank, out=torch.empty((B, Hq, D), dtype=torch.bfloat16))
