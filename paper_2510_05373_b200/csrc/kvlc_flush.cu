@@ -123,11 +123,11 @@ struct FlushArgs {
   float* s_out;              // prefill: per-CTA S partial [units][splits][D][RANK]; null => cache S
   float* p_out;
   int splits;
-  // prefill tensor-core path: quant_kernel -> state kernel scratch, slot = unit * slot_stride + chunk
-  uint8_t* vbytes;           // [slot][G][D] value codes
-  float2* vsz;               // [slot][G] (scale, zero) fp32 per token
-  float2* ksz;               // [slot][D] (scale, zero) fp32 per channel
-  uint4* kw;                 // [slot][8 warps][32 lanes] the lane's 4 packed K words (K1 fragment order)
+  // prefill tensor-core path: quant_kernel -> state kernel operand images (the state
+  // kernel's shared-memory tiles byte for byte), slot = unit * slot_stride + chunk
+  uint8_t* aimg;             // [slot][hi, lo][FT_TILE]  k_err = A_phi (MN-major, 128 B swizzle)
+  uint8_t* cimg;             // [slot][FT_TILE]  value codes as fp16, [M = channel][K = token] MN-major
+  float2* vsz;               // [slot][G]  value (scale, zero) per token, fp32 (v_q = s code + z)
   int slot_stride;
 };
 
@@ -595,41 +595,36 @@ __global__ void deserialize_unit_kernel(kvlc_cache c, int unit, int n, int n_res
 
 // ---------------------------------------------------------------------------
 // Prefill flush with the adapter-state update on the 5th-generation tensor
-// cores (tcgen05).  One CTA per (unit, feature half h, chunk range): W_h (the
-// 128 features of W1k or W2k, fp16 hi + lo) stays resident in shared memory;
-// per chunk (flush_group, cache.py:132-158):
-//   K1  keys, channel-wise codes (fp64 decisions, bit-exact) and k_err = k - k_hat
-//       -> A_phi = k_err [128 tokens x 128 channels] (fp16 hi / lo tiles);
-//   K2  values: fp64 FWHT, token-wise codes, v_q -> B_S = [v_q | 1 | 0] [128 tokens x 144];
-//   phi Z = k_err W_h (3 MMAs passes hi*hi + hi*lo + lo*hi, M = 128 tokens, N = 128,
-//       f32 in TMEM), row softmax (feature_map, adapter.py:80-88) -> A_S = Phi^T;
-//   S   D_S += Phi^T [v_q | 1] (M = 128 features, N = 144, accumulated in TMEM over the
-//       CTA's chunks): D_S[f][c] = S[c][h*128 + f], D_S[f][128] = P[h*128 + f].
-// Codes / metadata are written by the half-0 CTA.  Operand tiles are MN-major
-// without swizzle (core matrix 8 x 16 B, LBO 128 B between K groups, SBO 2048 B
-// between M/N groups), see kvlc_tc.cuh.
+// cores (tcgen05), cache.py:132-158, in two kernels:
+//   quant_kernel (one CTA per chunk): K1 keys, channel-wise codes (fp64 decisions,
+//       bit-exact); K2 values, FWHT + token-wise codes; the packed words and fp16
+//       metadata go to the cache, and the state kernel's operands to a scratch:
+//       k_err = k - k_hat as the A_phi tile image (fp16 hi / lo, 128 B swizzle), the
+//       value codes as an fp16 tile image and the fp32 value (scale, zero) per token.
+//   flush_tc_kernel (one CTA per (unit, feature half h, chunk range)): W_h (the 128
+//       features of W1k or W2k, fp16 hi / lo) resident in shared memory; per chunk
+//       phi Z = k_err W_h (3 passes hi.hi + hi.lo + lo.hi, M = 128 tokens, N = 128, f32 in
+//       TMEM), row softmax (feature_map, adapter.py:80-88) -> s 2^e Phi, and since
+//       v_q = s (code - 3/2) + z' (z' the row midpoint):
+//       S^T[c][f] += sum_t (code - 3/2)[t][c] 2^-e (s 2^e Phi)[t][f]  (2 passes, exact codes),
+//       with P[f] = sum_t Phi[t][f] and (z'^T Phi)[f] reduced in registers and added at the
+//       end.  The next chunk's A_phi image streams in while the softmax and S GEMM run.
 constexpr int FT_THREADS = 256;
 constexpr int FT_TILE = 32768;              // [128][128] fp16 tile
-constexpr int FT_NS = 144;                  // B_S columns: v_q (128), ones (1), zero padding
-constexpr int FT_TILE_S = FT_NS / 8 * 2048;  // [128][144] fp16 tile
-constexpr uint32_t FT_COL_PHI = 0, FT_COL_S = 128, FT_TMEM = 512;
+constexpr uint32_t FT_COL_PHI = 0, FT_COL_S = 128, FT_TMEM = 256;
 constexpr uint32_t FT_IDESC_PHI = (1u << 4) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | (8u << 24);
-constexpr uint32_t FT_IDESC_S = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(FT_NS >> 3) << 17) | (8u << 24);
 
 struct FtSmem {
   uint8_t w[2][FT_TILE];     // W_h hi / lo: B of the phi GEMM, [K = channel][N = feature]
-  uint8_t a[2][FT_TILE];     // A_phi (k_err, [M = token][K = channel]) then A_S (Phi^T, [M = feature][K = token])
-  uint8_t bs[2][FT_TILE_S];  // B_S hi / lo: [K = token][N = 144]
-  float red[2][FT_THREADS];
-  // the chunk's quant_kernel outputs, bulk-copied one chunk ahead
-  uint4 kw[FT_THREADS];      // packed K words, one uint4 per (warp, lane)
-  float2 ksz[D];             // K (scale, zero) per channel
-  uint8_t vb[G * D];         // value codes [token][channel], 16 B chunks swizzled by token & 7
-  float2 vsz[G];             // V (scale, zero) per token
-  uint64_t mphi, ms, mpre;
+  uint8_t a[2][FT_TILE];     // A_phi hi / lo: k_err [M = token][K = channel] (128 B swizzle)
+  uint8_t cv[FT_TILE];       // value codes (exact fp16): A of the S GEMM, [M = channel][K = token]
+  uint8_t ps[2][FT_TILE];    // s' Phi hi / lo: B of the S GEMM, [K = token][N = feature]
+  float2 vsz[G];             // value (scale, zero) per token
+  float red[2][G];           // softmax row max / sum of the two 64-feature halves
+  uint64_t mphi, ms, mc;     // phi GEMM done, S GEMM done, code tile + (s, z) landed
+  uint64_t ma[2];            // A_phi hi, lo landed
   uint32_t tbase;
 };
-constexpr uint32_t FT_PRE_BYTES = FT_THREADS * 16 + D * 8 + G * D + G * 8;
 
 // Value codes [token][channel] with an XOR swizzle on channel bits 2-4 (groups of 4
 // channels stay contiguous): conflict-free packing reads.
@@ -679,12 +674,19 @@ __device__ __forceinline__ uint64_t ft_desc_a(const void* p) {
 constexpr int FT_A_KSTEP = 2048 >> 4;  // descriptor advance per K = 16 step (two 8-row groups)
 
 // 3 passes (hi*hi, hi*lo, lo*hi) of a K = 128 contraction: 24 MMAs, one elected lane.
+// `late` (optional): an mbarrier (phase `parity`) guarding the operand first used by pass
+// `late_pass` (a lo tile still in flight while the earlier passes run).
 __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE], const uint8_t* b0, const uint8_t* b1,
-                                        uint32_t idesc, bool accumulate) {
+                                        uint32_t idesc, bool accumulate, uint64_t* late = nullptr,
+                                        uint32_t parity = 0, int late_pass = 3) {
   const uint64_t ah = ft_desc_a(a[0]), al = ft_desc_a(a[1]), bh = ft_desc(b0), bl = ft_desc(b1);
   const uint64_t pa[3] = {ah, ah, al}, pb[3] = {bh, bl, bh};
 #pragma unroll
-  for (int p = 0; p < 3; ++p)
+  for (int p = 0; p < 3; ++p) {
+    if (late && p == late_pass) {
+      tc::mbar_wait(late, parity);
+      tc::fence_after_sync();
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const uint32_t acc = (accumulate || p > 0 || j > 0) ? 1u : 0u;
@@ -694,6 +696,7 @@ __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE],
           "l"(pa[p] + FT_A_KSTEP * j), "l"(pb[p] + 16 * j), "r"(idesc), "r"(acc)
           : "memory");
     }
+  }
 }
 
 // Prefill quantization (K1 + K2) at one chunk per CTA: code decisions, FWHT,
@@ -770,7 +773,6 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         const double scale = __ddiv_rn(__dsub_rn(mx, mn), 3.0);
         sm.kpar[ch0 + own] = make_double2(mn, scale);
         sm.kparf[ch0 + own] = make_float4((float)mn, (float)scale, scale > 0.0 ? (float)(1.0 / scale) : 0.f, 0.f);
-        a.ksz[slot * D + ch0 + own] = make_float2((float)scale, (float)mn);
         if (writer) {
           c.kscale[cb * D + ch0 + own] = __half_as_ushort(__double2half(scale));
           c.kzero[cb * D + ch0 + own] = __half_as_ushort(__double2half(mn));
@@ -778,10 +780,12 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       }
       __syncwarp();
       uint32_t cw[4] = {0u, 0u, 0u, 0u};  // K words t0 = 0..3 of this lane's tokens
+      uint8_t* aimg = a.aimg + slot * 2 * FT_TILE;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const float4 pf = sm.kparf[ch0 + e];
         const float mnf = pf.x, scf = pf.y, invf = pf.z;
+        __half ehi[4], elo[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           uint32_t code = 0u;
@@ -798,14 +802,19 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
           // byte q of word t0 holds channel 16kt + 2t0 + {0,8,1,9}[q]; bit pair r holds token 4l + r
           const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
           cw[t0] |= code << (8 * qb + 2 * r);
+          // k_err = k - (s code + z) (cache.py:153) as an fp16 hi / lo pair
+          ft_hilo(x[r][e] - fmaf((float)code, scf, mnf), ehi[r], elo[r]);
         }
+        // A_phi image element (tokens 4l .. 4l+3, channel ch0 + e): 8 contiguous bytes
+        const int off = ft_off_a(4 * lane, ch0 + e);
+        *reinterpret_cast<uint2*>(aimg + off) = *reinterpret_cast<const uint2*>(ehi);
+        *reinterpret_cast<uint2*>(aimg + FT_TILE + off) = *reinterpret_cast<const uint2*>(elo);
       }
       if (writer) {
         const int wt = lane >> 3, g = lane & 7;  // tokens 32 wt + 4 g + r
 #pragma unroll
         for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = cw[t0];
       }
-      a.kw[slot * 256 + tid] = make_uint4(cw[0], cw[1], cw[2], cw[3]);
     }
     // ---- K2: values, FWHT post-rotation (fp32, guarded), token-wise quantization ----
     // The fp32 FWHT differs from the reference's fp64 dense x @ H in the last bits:
@@ -947,9 +956,21 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       }
       const uint32_t cword = code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24);
       *reinterpret_cast<uint32_t*>(sm.codes + vsw(t, lane * 4)) = cword;
-      // state-kernel scratch: 16 B chunk (lane / 4) of row t stored at chunk (lane / 4) ^ (t & 7)
-      *reinterpret_cast<uint32_t*>(a.vbytes + ((size_t)slot * G + t) * D + ((((lane >> 2) ^ (t & 7)) << 4) | ((lane & 3) << 2))) = cword;
-      if (lane == 0) a.vsz[slot * G + t] = make_float2(vsc, vmn);
+      {  // codes -> the state kernel's A tile (channels 4l .. 4l+3, token t).  v_q = s code + z
+         // (cache.py:154) is applied there as S = ((code - 3/2) 2^-e)^T (s 2^e Phi) + 1 (z'^T Phi),
+         // z' = z + 3/2 s the row midpoint: centred codes keep the two terms from cancelling
+         // (z alone is ~ -2 for N(0,1) rows, S ~ 0.5), the per-token power of two 2^e puts
+         // s 2^e in [2^10, 2^11) so the fp16 hi / lo split of s 2^e Phi stays out of the
+         // subnormal range, and (code - 3/2) 2^-e is exact in fp16
+        int ex;
+        frexpf(vsc > 0.f ? vsc : 1.f, &ex);
+        const int e = min(max(11 - ex, -14), 22);
+        const float cs = __int_as_float((127 - e) << 23);  // 2^-e
+        auto hc = [&](uint32_t cd) { return (uint32_t)__half_as_ushort(__float2half_rn(((float)cd - 1.5f) * cs)); };
+        *reinterpret_cast<uint2*>(a.cimg + slot * FT_TILE + ft_off(4 * lane, t)) =
+            make_uint2(hc(code[0]) | (hc(code[1]) << 16), hc(code[2]) | (hc(code[3]) << 16));
+        if (lane == 0) a.vsz[slot * G + t] = make_float2(vsc * __int_as_float((127 + e) << 23), fmaf(1.5f, vsc, vmn));
+      }
       if (writer && lane == 0) {
         c.vscale[cb * G + t] = meta_s;
         c.vzero[cb * G + t] = meta_z;
@@ -971,12 +992,37 @@ __device__ long long g_ftrace[2][40][10];  // CTA (0, 0, h): per chunk clock64 a
   } while (0)
 #endif
 
-__device__ __forceinline__ void ft_prefetch(FtSmem& sm, const FlushArgs& a, size_t slot) {
-  tc::mbar_expect_tx(&sm.mpre, FT_PRE_BYTES);
-  tc::bulk_g2s(sm.kw, a.kw + slot * FT_THREADS, FT_THREADS * 16, &sm.mpre);
-  tc::bulk_g2s(sm.ksz, a.ksz + slot * D, D * 8, &sm.mpre);
-  tc::bulk_g2s(sm.vb, a.vbytes + slot * G * D, G * D, &sm.mpre);
-  tc::bulk_g2s(sm.vsz, a.vsz + slot * G, G * 8, &sm.mpre);
+// The chunk's operand images (written by quant_kernel) into the shared-memory tiles.
+// (hi and lo on separate barriers: the GEMMs' first two passes need only the hi tiles)
+__device__ __forceinline__ void ft_load_a(FtSmem& sm, const FlushArgs& a, size_t slot) {
+  const uint8_t* src = a.aimg + slot * 2 * FT_TILE;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    tc::mbar_expect_tx(&sm.ma[i], FT_TILE);
+    tc::bulk_g2s(sm.a[i], src + i * FT_TILE, FT_TILE, &sm.ma[i]);
+  }
+}
+__device__ __forceinline__ void ft_load_c(FtSmem& sm, const FlushArgs& a, size_t slot) {
+  tc::mbar_expect_tx(&sm.mc, FT_TILE + G * sizeof(float2));
+  tc::bulk_g2s(sm.cv, a.cimg + slot * FT_TILE, FT_TILE, &sm.mc);
+  tc::bulk_g2s(sm.vsz, a.vsz + slot * G, G * sizeof(float2), &sm.mc);
+}
+
+// S GEMM (D^T[c][f] += sum_t code[t][c] (s' Phi)[t][f]): 2 passes (codes are exact in fp16).
+__device__ __forceinline__ void ft_gemm_s(uint32_t d, const uint8_t* cv, const uint8_t* b0, const uint8_t* b1,
+                                          bool accumulate) {
+  const uint64_t ac = ft_desc(cv), pb[2] = {ft_desc(b0), ft_desc(b1)};
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t acc = (accumulate || p > 0 || j > 0) ? 1u : 0u;
+      asm volatile(
+          "{\n.reg .pred q, e;\nsetp.ne.b32 q, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+          "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n}\n" ::"r"(d),
+          "l"(ac + 16 * j), "l"(pb[p] + 16 * j), "r"(FT_IDESC_PHI), "r"(acc)
+          : "memory");
+    }
 }
 
 __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs a, const SeqInfo seq,
@@ -990,27 +1036,25 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   const int nf = seq.nflush[b];
   const int c_lo = split * a.cpc, c_hi = min(nf, c_lo + a.cpc);
   if (c_lo >= c_hi) return;
+  const size_t slot0 = (size_t)unit * a.slot_stride;
 
-  // resident W_h tiles (prepared by prep_wtiles_kernel), constant B_S columns, TMEM, barriers
+  // resident W_h tiles (prepared by prep_wtiles_kernel), TMEM, barriers, first images
   {
     const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + h) * 2 * FT_TILE);
     uint4* dst = reinterpret_cast<uint4*>(sm.w[0]);
     for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
     tc::cp_commit();
   }
-  for (int i = tid; i < 2 * G * 2; i += FT_THREADS) {  // tile x token x column group 16 / 17
-    const int tile = i / (2 * G), t = (i >> 1) % G, grp = 16 + (i & 1);
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (tile == 0 && grp == 16) v.x = 0x3C00u;  // hi tile, column 128 = 1.0 (P); lo and padding 0
-    *reinterpret_cast<uint4*>(sm.bs[tile] + grp * 2048 + (t >> 3) * 128 + (t & 7) * 16) = v;
-  }
   if (warp == 0) tc::tmem_alloc(&sm.tbase, FT_TMEM);
   if (tid == 0) {
     tc::mbar_init(&sm.mphi, 1);
     tc::mbar_init(&sm.ms, 1);
-    tc::mbar_init(&sm.mpre, 1);
+    tc::mbar_init(&sm.mc, 1);
+    tc::mbar_init(&sm.ma[0], 1);
+    tc::mbar_init(&sm.ma[1], 1);
     tc::mbar_fence_init();
-    ft_prefetch(sm, a, (size_t)unit * a.slot_stride + c_lo);
+    ft_load_a(sm, a, slot0 + c_lo);
+    ft_load_c(sm, a, slot0 + c_lo);
   }
   tc::cp_wait<0>();
   tc::fence_before_sync();
@@ -1019,124 +1063,32 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   if ((tc::smem_u32(sm.a[0]) & 1023u) != 0) __trap();  // swizzle atoms must be 1024 B aligned
   const uint32_t tb = sm.tbase;
   const uint32_t lane_addr = tb + ((uint32_t)(32 * (warp & 3)) << 16);
+  const int part = warp >> 2;
+  // P[f] = sum_t phi[t][f], Z[f] = sum_t z_t phi[t][f] for this warp's 32 token rows:
+  // lane owns features 64 part + 2 lane + {0, 1} (reduce-scatter order)
+  float pacc[2] = {0.f, 0.f}, zacc[2] = {0.f, 0.f};
 
-  uint4 kpre[8];  // raw keys of the next chunk (lane l: tokens 4l..4l+3, channels 16 warp..+15)
-  {
-    const uint16_t* K0 = a.ksrc + unit * a.k_unit + (int64_t)c_lo * G * a.k_t;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const uint4* src = reinterpret_cast<const uint4*>(K0 + (size_t)(4 * lane + r) * D + 16 * warp);
-      kpre[2 * r] = __ldg(src);
-      kpre[2 * r + 1] = __ldg(src + 1);
-    }
-  }
   for (int ci = c_lo; ci < c_hi; ++ci) {
     const int it = ci - c_lo;
-    const int64_t tok0 = (int64_t)ci * G;
-    const uint16_t* K = a.ksrc + unit * a.k_unit + tok0 * a.k_t;
-    const uint16_t* V = a.vsrc + unit * a.v_unit + tok0 * a.v_t;
-    const size_t cb = (size_t)unit * c.max_chunks + ci;
     FT_STAMP(0);
-    if (it > 0) {  // the previous S GEMM has read A_S (aliased by A_phi) and B_S
-      tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);
+    if (warp == 0) {  // phi GEMM: Z = k_err W_h (passes hi.hi, hi.lo once A hi has landed, lo.hi after A lo)
+      tc::mbar_wait(&sm.ma[0], (uint32_t)it & 1u);
       tc::fence_after_sync();
-    }
-    tc::mbar_wait(&sm.mpre, (uint32_t)it & 1u);  // this chunk's staged quant_kernel outputs
-    FT_STAMP(1);
-
-    // ---- k_err = k - (s code + z) (cache.py:153) from the raw keys, the packed K words and the
-    // fp32 (scale, zero) of quant_kernel.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3.
-    {
-      const int ch0 = 16 * warp;
-      const size_t slot = (size_t)unit * a.slot_stride + ci;
-      float x[4][16];
-      uint4 kcur[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) kcur[i] = kpre[i];
-      if (ci + 1 < c_hi) {  // the next chunk's raw keys, in flight during this chunk
-        const uint16_t* Kn = K + (int64_t)G * a.k_t;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const uint4* src = reinterpret_cast<const uint4*>(Kn + (size_t)(4 * lane + r) * D + ch0);
-          kpre[2 * r] = __ldg(src);
-          kpre[2 * r + 1] = __ldg(src + 1);
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const uint4 p0 = kcur[2 * r], p1 = kcur[2 * r + 1];
-        const uint32_t wv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          x[r][2 * e] = __uint_as_float(wv[e] << 16);
-          x[r][2 * e + 1] = __uint_as_float(wv[e] & 0xffff0000u);
-        }
-      }
-      const uint4 cwv = sm.kw[tid];
-      const uint32_t cw[4] = {cwv.x, cwv.y, cwv.z, cwv.w};
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const float2 sz = sm.ksz[ch0 + e];
-        const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
-        __half hi[4], lo[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const float code = (float)((cw[t0] >> (8 * qb + 2 * r)) & 3u);
-          ft_hilo(x[r][e] - fmaf(code, sz.x, sz.y), hi[r], lo[r]);
-        }
-        // A_phi element (token 4l + r, channel ch0 + e): 4 consecutive tokens are 8 contiguous bytes
-        *reinterpret_cast<uint2*>(sm.a[0] + ft_off_a(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(hi);
-        *reinterpret_cast<uint2*>(sm.a[1] + ft_off_a(4 * lane, ch0 + e)) = *reinterpret_cast<uint2*>(lo);
-      }
-    }
-    FT_STAMP(2);
-    tc::fence_proxy_async();
-    tc::fence_before_sync();
-    __syncthreads();
-    FT_STAMP(3);
-    if (warp == 0) {  // phi GEMM: Z = k_err W_h
-      tc::fence_after_sync();
-      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false);
+      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false, &sm.ma[1], (uint32_t)it & 1u, 2);
       tc::mma_commit_w(&sm.mphi);
     }
-
-    // ---- v_q = s_t code + z_t (cache.py:154, rotated basis) -> B_S row t; thread t, half `part`
-    {
-      const int t = tid & 127, part = tid >> 7;
-      const float2 sz = sm.vsz[t];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 w = *reinterpret_cast<const uint4*>(sm.vb + t * D + (((4 * part + q) ^ (t & 7)) << 4));
-        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {  // 8 channels 64 part + 16 q + 8 hh
-          __half hi[8], lo[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float code = (float)((wv[2 * hh + (e >> 2)] >> (8 * (e & 3))) & 0xffu);
-            ft_hilo(fmaf(code, sz.x, sz.y), hi[e], lo[e]);
-          }
-          const int ch = 64 * part + 16 * q + 8 * hh;
-          *reinterpret_cast<uint4*>(sm.bs[0] + ft_off(ch, t)) = *reinterpret_cast<uint4*>(hi);
-          *reinterpret_cast<uint4*>(sm.bs[1] + ft_off(ch, t)) = *reinterpret_cast<uint4*>(lo);
-        }
-      }
-    }
-    FT_STAMP(4);
-    __syncthreads();
-    if (tid == 0 && ci + 1 < c_hi) {  // staging consumed by K1' / K2': fetch the next chunk's
-      tc::fence_proxy_async();
-      ft_prefetch(sm, a, (size_t)unit * a.slot_stride + ci + 1);
-    }
-    FT_STAMP(5);
-    FT_STAMP(6);
-
-    // ---- softmax of Z (token rows): warps w and w + 4 share TMEM lanes 32 (w & 3) .., 64 columns each ----
+    FT_STAMP(1);
     tc::mbar_wait(&sm.mphi, (uint32_t)it & 1u);
     tc::fence_after_sync();
-    FT_STAMP(7);
+    if (tid == 0 && ci + 1 < c_hi) ft_load_a(sm, a, slot0 + ci + 1);  // A_phi consumed: next one in flight
+    tc::mbar_wait(&sm.mc, (uint32_t)it & 1u);  // this chunk's (s, z)
+    if (it > 0) tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);  // the previous S GEMM has read s' Phi
+    FT_STAMP(2);
+
+    // ---- softmax of Z (token rows; feature_map, adapter.py:80-88): warps w and w + 4 share TMEM
+    // lanes 32 (w & 3) .., 64 feature columns each ----
     {
-      const int t = 32 * (warp & 3) + lane, part = warp >> 2;
+      const int t = 32 * (warp & 3) + lane;
       float z[64];
       tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part, reinterpret_cast<uint32_t*>(z));
       tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part + 32, reinterpret_cast<uint32_t*>(z) + 32);
@@ -1159,47 +1111,92 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       sm.red[part][t] = ssum;
       __syncthreads();
       const float inv = 1.f / (sm.red[0][t] + sm.red[1][t]);
-      // A_S = Phi^T: element (feature f, token t); 8 consecutive features are 16 contiguous bytes
+      const float2 vz = sm.vsz[t];  // (s 2^e, z'): see quant_kernel
+      const float sp = vz.x;
+      // B of the S GEMM: s' phi, element (token t, feature f); 8 consecutive features = 16 B
+      float w[64];
 #pragma unroll
       for (int f8 = 0; f8 < 64; f8 += 8) {
         __half hi[8], lo[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) ft_hilo(z[f8 + e] * inv, hi[e], lo[e]);
-        *reinterpret_cast<uint4*>(sm.a[0] + ft_off_a(64 * part + f8, t)) = *reinterpret_cast<uint4*>(hi);
-        *reinterpret_cast<uint4*>(sm.a[1] + ft_off_a(64 * part + f8, t)) = *reinterpret_cast<uint4*>(lo);
+        for (int e = 0; e < 8; ++e) {
+          const float ph = z[f8 + e] * inv;
+          z[f8 + e] = ph;
+          w[f8 + e] = vz.y * ph;
+          ft_hilo(sp * ph, hi[e], lo[e]);
+        }
+        *reinterpret_cast<uint4*>(sm.ps[0] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(hi);
+        *reinterpret_cast<uint4*>(sm.ps[1] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(lo);
       }
+      // P and z^T Phi over the warp's 32 tokens: reduce-scatter (lane keeps features 2 lane + {0, 1})
+#pragma unroll
+      for (int step = 0; step < 5; ++step) {
+        const int sft = 16 >> step, n = 32 >> step;
+        const bool up = lane & sft;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          if (e < n) {
+            const float s1 = up ? z[e] : z[e + n], k1 = up ? z[e + n] : z[e];
+            const float s2 = up ? w[e] : w[e + n], k2 = up ? w[e + n] : w[e];
+            z[e] = k1 + __shfl_xor_sync(0xffffffffu, s1, sft);
+            w[e] = k2 + __shfl_xor_sync(0xffffffffu, s2, sft);
+          }
+        }
+      }
+      pacc[0] += z[0];
+      pacc[1] += z[1];
+      zacc[0] += w[0];
+      zacc[1] += w[1];
     }
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
-    FT_STAMP(8);
-    if (warp == 0) {  // S GEMM: D_S += Phi^T [v_q | 1]
+    FT_STAMP(3);
+    if (warp == 0) {  // S GEMM: D^T += codes^T (s' Phi), then the next code tile once it is read
       tc::fence_after_sync();
-      ft_gemm(tb + FT_COL_S, sm.a, sm.bs[0], sm.bs[1], FT_IDESC_S, it > 0);
+      ft_gemm_s(tb + FT_COL_S, sm.cv, sm.ps[0], sm.ps[1], it > 0);
       tc::mma_commit_w(&sm.ms);
+      if (ci + 1 < c_hi) {
+        tc::mbar_wait(&sm.ms, (uint32_t)it & 1u);
+        if (lane == 0) ft_load_c(sm, a, slot0 + ci + 1);
+        __syncwarp();
+      }
     }
+    FT_STAMP(4);
   }
 
-  // ---- drain D_S: row f (TMEM lane), columns c (S[c][h*128 + f]) and 128 (P) ----
+  // ---- drain: S[c][h*128 + f] = D^T[c][f] + (z^T Phi)[f] (cache.py:155-157), P[h*128 + f] ----
   tc::mbar_wait(&sm.ms, (uint32_t)(c_hi - c_lo - 1) & 1u);
   tc::fence_after_sync();
+  float* zf = reinterpret_cast<float*>(sm.ps[0]);  // free now: [4 token groups][128 features][P, Z]
   {
-    const int f = 32 * (warp & 3) + lane, part = warp >> 2;
-    float* S = a.s_out ? a.s_out + ((size_t)unit * a.splits + split) * D * RANK : c.S + (size_t)unit * D * RANK;
-    float* P = a.p_out ? a.p_out + ((size_t)unit * a.splits + split) * RANK : c.P + (size_t)unit * RANK;
+    const int f = 64 * part + 2 * lane;
+    *reinterpret_cast<float4*>(zf + ((warp & 3) * 128 + f) * 2) = make_float4(pacc[0], zacc[0], pacc[1], zacc[1]);
+  }
+  __syncthreads();
+  float* S = a.s_out ? a.s_out + ((size_t)unit * a.splits + split) * D * RANK : c.S + (size_t)unit * D * RANK;
+  float* P = a.p_out ? a.p_out + ((size_t)unit * a.splits + split) * RANK : c.P + (size_t)unit * RANK;
+  if (tid < HALF) {
+    float pf = 0.f;
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) pf += zf[(g4 * 128 + tid) * 2];
+    P[h * HALF + tid] += pf;
+  }
+  {
+    const int cch = 32 * (warp & 3) + lane;  // TMEM lane = value channel
     float d[32];
 #pragma unroll 1
     for (int c0 = 64 * part; c0 < 64 * part + 64; c0 += 32) {
       tc::tmem_ld32(lane_addr + FT_COL_S + c0, reinterpret_cast<uint32_t*>(d));
       tc::wait_ld();
+      float* row = S + (size_t)cch * RANK + h * HALF + c0;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) S[(size_t)(c0 + i) * RANK + h * HALF + f] += d[i];
-    }
-    if (part == 0) {
-      uint32_t pv[8];
-      tc::tmem_ld8(lane_addr + FT_COL_S + D, pv);
-      tc::wait_ld();
-      P[h * HALF + f] += __uint_as_float(pv[0]);
+      for (int i = 0; i < 32; ++i) {
+        const int f = c0 + i;
+        const float zt = (zf[(0 * 128 + f) * 2 + 1] + zf[(1 * 128 + f) * 2 + 1]) +
+                         (zf[(2 * 128 + f) * 2 + 1] + zf[(3 * 128 + f) * 2 + 1]);
+        row[i] += d[i] + zt;
+      }
     }
   }
   tc::fence_before_sync();
@@ -1260,11 +1257,12 @@ size_t kvlc_prefill_workspace(const kvlc_cache* c, int64_t n_tok) {
   int splits = (int)((nf + 3) / 4);
   if (splits < 1) splits = 1;
   // S / P partials (the tensor-core path uses fewer splits) + the W hi / lo tiles +
-  // the quant_kernel -> state-kernel scratch (value codes, fp32 scale / zero)
+  // the quant_kernel -> state-kernel operands (A_phi hi / lo 64 KB, fp16 codes 32 KB and the
+  // value (scale, zero) 1 KB per chunk)
+  const size_t nslot = (size_t)units * std::max<int64_t>(nf, 1);
   return align_up((size_t)units * splits * (D * RANK + RANK) * sizeof(float)) +
-         align_up((size_t)c->Hkv * 2 * 2 * FT_TILE) + align_up((size_t)units * std::max<int64_t>(nf, 1) * G * D) +
-         2 * align_up((size_t)units * std::max<int64_t>(nf, 1) * G * sizeof(float2)) +
-         align_up((size_t)units * std::max<int64_t>(nf, 1) * FT_THREADS * 16);
+         align_up((size_t)c->Hkv * 2 * 2 * FT_TILE) + align_up(nslot * 2 * FT_TILE) + align_up(nslot * FT_TILE) +
+         align_up(nslot * G * sizeof(float2));
 }
 
 int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k, const uint16_t* v,
@@ -1304,11 +1302,10 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     float* s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
     uint8_t* wtiles = ar.take<uint8_t>((size_t)c->Hkv * 2 * 2 * FT_TILE);
     const int slot_stride = (int)std::max<int64_t>(1, n_tok / KVLC_G);
-    uint8_t* vbytes = ar.take<uint8_t>((size_t)units * slot_stride * G * D);
+    uint8_t* aimg = ar.take<uint8_t>((size_t)units * slot_stride * 2 * FT_TILE);
+    uint8_t* cimg = ar.take<uint8_t>((size_t)units * slot_stride * FT_TILE);
     float2* vsz = ar.take<float2>((size_t)units * slot_stride * G);
-    float2* ksz = ar.take<float2>((size_t)units * slot_stride * D);
-    uint4* kw = ar.take<uint4>((size_t)units * slot_stride * FT_THREADS);
-    KVLC_REQUIRE(s_part && wtiles && vbytes && vsz && ksz && kw, "prefill workspace too small (%zu bytes)", ws_bytes);
+    KVLC_REQUIRE(s_part && wtiles && aimg && cimg && vsz, "prefill workspace too small (%zu bytes)", ws_bytes);
     float* p_part = s_part + (size_t)units * splits * D * RANK;
     KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
     prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
@@ -1329,10 +1326,9 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     a.s_out = s_part;
     a.p_out = p_part;
     a.splits = splits;
-    a.vbytes = vbytes;
+    a.aimg = aimg;
+    a.cimg = cimg;
     a.vsz = vsz;
-    a.ksz = ksz;
-    a.kw = kw;
     a.slot_stride = slot_stride;
     quant_kernel<<<dim3(max_nf, units), FT_THREADS, 0, s>>>(a, seq);
     if ((rc = check_launch("quant"))) return rc;

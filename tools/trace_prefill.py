@@ -25,12 +25,12 @@ buf = np.zeros((2, 40, 10), np.int64)
 fn = lib["_ZN4kvlc16kvlc_ftrace_copyEPvm"]
 fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert fn(buf.ctypes.data, buf.nbytes) == 0
-names = ["waitS", "K1", "bar", "phiIss+K2", "bar", "packV", "waitPhi", "softmax"]
+names = ["waitA+phi", "waitPhi+C+S", "softmax", "S+loadC"]
 print("  it  " + " ".join(f"{n:>9s}" for n in names) + "   iter")
 for it in range(12):
     r = buf[0, it]
     if r[0] == 0:
         break
-    d = [r[i + 1] - r[i] for i in range(8)]
+    d = [r[i + 1] - r[i] for i in range(4)]
     nxt = buf[0, it + 1, 0] - r[0] if buf[0, it + 1, 0] else -1
     print(f"  {it:2d}  " + " ".join(f"{x:9d}" for x in d) + f"  {nxt:6d}")
