@@ -47,21 +47,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// same, with an L2 evict-first hint (the cache codes are streamed once per step)
-__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                                uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
-      "%4;\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-
 // ---------------------------------------------------------------- cp.async (LDGSTS)
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
@@ -89,11 +74,6 @@ __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.
 // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
-               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
-}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -121,17 +101,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr)
       : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-}
-
 // ---------------------------------------------------------------- MMA
-// kind::f16, f32 accumulate, A K-major (TMEM), B MN-major, M = 128, N = 16.
+// kind::f16, f32 accumulate, A K-major (TMEM), B MN-major, M = 128, N = 16 (the A-in-TMEM
+// forms below back the latency / issue probes in tools/microbench).
 constexpr uint32_t IDESC_F16_M128_N16 = (1u << 4) | (1u << 16) | (2u << 17) | (8u << 24);
 
 // Shared-memory matrix descriptor, no swizzle, LBO = 128 B, SBO = 2048 B.
@@ -143,17 +115,6 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %3, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, p;\n}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(accumulate), "r"(IDESC_F16_M128_N16)
-      : "memory");
-}
-// Warp-uniform forms: the whole warp executes the call, elect.sync picks the
-// issuing lane inside the asm.  (Issuing from a divergent `if (lane == 0)`
-// makes the compiler wrap every uniform-datapath instruction in an ELECT
-// loop: ~44 cycles per MMA instead of ~10 — tools/microbench/umma_latency.cu.)
-__device__ __forceinline__ void mma_f16_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %3, 0;\nelect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, p;\n}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(accumulate), "r"(IDESC_F16_M128_N16)
       : "memory");
 }
@@ -183,66 +144,10 @@ __device__ __forceinline__ void mma8_commit_w(uint32_t d_tmem, uint32_t a_tmem, 
       "r"(a_tmem), "l"(b_desc), "r"(IDESC_F16_M128_N16), "r"(smem_u32(bar))
       : "memory");
 }
-// QK of one chunk: D = sum_j A_K[:, 8j..] B_QK[16j..] + sum_j A_ones B_Z[16j..]
-// (the second chain adds the key zero term sum_c q_c z_c to every row), then a
-// commit to `bar`; one elected lane of the calling warp.
-__device__ __forceinline__ void mma16_qk_commit_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t a_ones,
-                                                  uint64_t z_desc, uint64_t* bar) {
-  asm volatile(
-      "{\n.reg .pred e, t, f;\n.reg .b32 a<8>;\n.reg .b64 b<8>, z<8>;\n"
-      "setp.ne.b32 t, 1, 0;\nsetp.ne.b32 f, 0, 0;\n"
-      "add.u32 a1, %1, 8;\nadd.u32 a2, %1, 16;\nadd.u32 a3, %1, 24;\nadd.u32 a4, %1, 32;\n"
-      "add.u32 a5, %1, 40;\nadd.u32 a6, %1, 48;\nadd.u32 a7, %1, 56;\n"
-      "add.u64 b1, %2, 16;\nadd.u64 b2, %2, 32;\nadd.u64 b3, %2, 48;\nadd.u64 b4, %2, 64;\n"
-      "add.u64 b5, %2, 80;\nadd.u64 b6, %2, 96;\nadd.u64 b7, %2, 112;\n"
-      "add.u64 z1, %5, 16;\nadd.u64 z2, %5, 32;\nadd.u64 z3, %5, 48;\nadd.u64 z4, %5, 64;\n"
-      "add.u64 z5, %5, 80;\nadd.u64 z6, %5, 96;\nadd.u64 z7, %5, 112;\n"
-      "elect.sync _|e, 0xffffffff;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, f;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %5, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], z1, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], z2, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], z3, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], z4, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], z5, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], z6, %3, t;\n"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], z7, %3, t;\n"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n"
-      "}\n" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(IDESC_F16_M128_N16), "r"(a_ones), "l"(z_desc), "r"(smem_u32(bar))
-      : "memory");
-}
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
-      : "memory");
-}
-// expect_tx(bytes) on `bar`, then two 4 KB and four 256 B bulk copies (one
-// decode chunk), all from one elected lane; evict-first L2 policy.
-__device__ __forceinline__ void bulk_chunk_w(uint64_t* bar, uint32_t bytes, void* d0, const void* s0, void* d1,
-                                             const void* s1, void* d2, const void* s2, void* d3, const void* s3,
-                                             void* d4, const void* s4, void* d5, const void* s5) {
-  asm volatile(
-      "{\n.reg .pred e;\n.reg .b64 pol;\nelect.sync _|e, 0xffffffff;\n"
-      "@e createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%2], [%3], 4096, [%0], pol;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%4], [%5], 4096, [%0], pol;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%6], [%7], 256, [%0], pol;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%8], [%9], 256, [%0], pol;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%10], [%11], 256, [%0], pol;\n"
-      "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%12], [%13], 256, [%0], pol;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(bytes), "r"(smem_u32(d0)), "l"(s0), "r"(smem_u32(d1)), "l"(s1), "r"(smem_u32(d2)), "l"(s2),
-      "r"(smem_u32(d3)), "l"(s3), "r"(smem_u32(d4)), "l"(s4), "r"(smem_u32(d5)), "l"(s5)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
