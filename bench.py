@@ -312,7 +312,7 @@ def run_other_configs(dev, peak_gbs):
     out["config5_qwen3-8b_prefill_32k"] = {
         "us_per_step": ms * 1e3, "kv_head_tokens_per_s": b * hkv * n / (ms * 1e-3),
         "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "roofline_frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs,
-        "kernel": "flush_tc_kernel: tcgen05 3-pass fp16 phi_k / S,P GEMMs (TMEM accumulators)"}
+        "kernel": "quant_kernel (codes, FWHT, operand images) + flush_tc_kernel (tcgen05: 3-pass fp16 phi_k GEMM, 2-pass S GEMM on exact codes, TMEM accumulators)"}
     return out
 
 
