@@ -13,7 +13,7 @@ is `paper_2510_05373_b200.batched` / `.distributed`.
 """
 from .adapter import (CorrectionAdapter, correction_term, feature_map, phi_k, phi_q,  # noqa: F401
                       rng)
-from .attention import DecodePartial, decode_step_blocked  # noqa: F401
+from .attention import DecodePartial, decode_step_blocked, quantize_roundtrip  # noqa: F401
 from .cache import (CacheFormatError, FootprintReport, KVCacheState, deserialize_cache,  # noqa: F401
                     memory_footprint, read_cache, serialize_cache, write_cache)
 from .hadamard import HadamardMatrix, hadamard_matrix, rotate  # noqa: F401
@@ -25,7 +25,7 @@ __version__ = "1.0.0"
 
 __all__ = [
     "CorrectionAdapter", "correction_term", "feature_map", "phi_q", "phi_k", "rng",
-    "DecodePartial", "decode_step_blocked",
+    "DecodePartial", "decode_step_blocked", "quantize_roundtrip",
     "FootprintReport", "KVCacheState", "memory_footprint", "serialize_cache", "deserialize_cache",
     "read_cache", "write_cache", "CacheFormatError",
     "HadamardMatrix", "hadamard_matrix", "rotate",

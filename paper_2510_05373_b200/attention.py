@@ -17,6 +17,8 @@ from . import _lib
 from ._device import empty_dev, to_dev, to_host
 from .adapter import CorrectionAdapter
 from .cache import KVCacheState
+from .hadamard import hadamard_matrix, rotate
+from .quantize import QuantConfig, quantize_tensor
 
 
 @dataclass
@@ -71,3 +73,25 @@ def decode_step_blocked(q, cache: KVCacheState, adapter: CorrectionAdapter | Non
         return out, DecodePartial(y_partial=to_host(py[:nb], "f32"), block_max=to_host(pm[:nb], "f32"),
                                   block_sum=to_host(pl[:nb], "f32"))
     return out
+
+
+def quantize_roundtrip(x, cfg: QuantConfig) -> np.ndarray:
+    """Rotate per config, quantize, dequantize, rotate back (attention.py:68-88): the
+    matrix attention sees after storage, in the original basis; bits = 16 skips the
+    quantization.  Every step runs on the device (kvlc_ref_rotate / _quantize /
+    _dequantize); H is symmetric, so rotating back is the same rotation."""
+    x = np.asarray(x, dtype=np.float64)
+    if cfg.rotation == "pre":
+        h = hadamard_matrix(x.shape[0])
+        xr = rotate(x, h, "pre")
+    elif cfg.rotation == "post":
+        h = hadamard_matrix(x.shape[1])
+        xr = rotate(x, h, "post")
+    else:
+        h, xr = None, x
+    xq = xr if cfg.is_passthrough else quantize_tensor(xr, cfg).dequantize()
+    if cfg.rotation == "pre":
+        return rotate(xq, h, "pre")
+    if cfg.rotation == "post":
+        return rotate(xq, h, "post")
+    return xq

@@ -266,3 +266,25 @@ def test_exact_keys_give_uniform_feature_states():
     v_q = cache.dequantized_values(0, n)
     want = np.outer(v_q.sum(axis=0), np.full(rank, 2.0 / rank))
     assert np.max(np.abs(cache.s_state - want)) <= 1e-12
+
+
+@pytest.mark.parametrize("rotation,bits,shape", [("post", 2, (40, 64)), ("pre", 4, (32, 24)), ("none", 3, (17, 30)),
+                                                 ("post", 16, (8, 16))])
+def test_quantize_roundtrip_matches_reference_composition(rotation, bits, shape):
+    """quantize_roundtrip (attention.py:68-88): rotate, quantize, dequantize, rotate back."""
+    from oracle import kvlinc_oracle as orc
+    x = orc.rng(7).standard_normal(shape)
+    axis = "channel" if rotation == "pre" else "token"
+    cfg = qk.QuantConfig(bits=bits, group_size=16, axis=axis, rotation=rotation)
+    got = qk.quantize_roundtrip(x, cfg)
+    if rotation == "pre":
+        h = orc.hadamard(shape[0])
+        xr = h @ x
+    elif rotation == "post":
+        h = orc.hadamard(shape[1])
+        xr = x @ h
+    else:
+        h, xr = None, x
+    xq = xr if bits == 16 else orc.dequantize_matrix(orc.quantize_matrix(xr, bits, 16, axis))
+    want = h.T @ xq if rotation == "pre" else (xq @ h.T if rotation == "post" else xq)
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.abs(want).max())
