@@ -496,25 +496,39 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
   const int unit = b * a.c.Hkv + kvh, qh = kvh * NG + h_local, gw = b * a.c.Hq + qh;
   const float* base = a.rec + (size_t)unit * a.nrec * NG * REC + (size_t)h_local * REC;
   const size_t rstride = (size_t)NG * REC;
-  float M = -INFINITY, Mt = -INFINITY;
-  for (int r0 = 0; r0 < a.nrec; r0 += 32) {
-    const int r = r0 + lane;
-    if (r < a.nrec) {
-      M = fmaxf(M, __ldcg(base + r * rstride));
-      Mt = fmaxf(Mt, __ldcg(base + r * rstride + 2));
-    }
+  // record headers (m, l, m_true, -): lane r holds records r, r + 32 (<= 64 records per
+  // unit, the planner's cap of 52 plus the residual halves), one load round for the max
+  // and the weights
+  float4 hd[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int r = 32 * j + lane;
+    hd[j] = r < a.nrec ? __ldcg(reinterpret_cast<const float4*>(base + r * rstride))
+                       : make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
   }
-  M = warp_max(M);
-  Mt = warp_max(Mt);
+  for (int r = 64 + lane; r < a.nrec; r += 32) {  // longer plans (explicit chunks_per_split)
+    const float4 x = __ldcg(reinterpret_cast<const float4*>(base + r * rstride));
+    hd[1].x = fmaxf(hd[1].x, x.x);
+    hd[1].z = fmaxf(hd[1].z, x.z);
+  }
+  float M = warp_max(fmaxf(hd[0].x, hd[1].x));
+  const float Mt = warp_max(fmaxf(hd[0].z, hd[1].z));
   float nr[4] = {0.f, 0.f, 0.f, 0.f}, nw[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
   if (M != -INFINITY) {
     for (int r0 = 0; r0 < a.nrec; r0 += 32) {
       const int r = r0 + lane, cnt = min(32, a.nrec - r0);
       float w = 0.f;
       if (r < a.nrec) {
-        const float m = __ldcg(base + r * rstride);
+        float m, l;
+        if (r0 < 64) {
+          m = r0 == 0 ? hd[0].x : hd[1].x;
+          l = r0 == 0 ? hd[0].y : hd[1].y;
+        } else {
+          m = __ldcg(base + r * rstride);
+          l = __ldcg(base + r * rstride + 1);
+        }
         w = m == -INFINITY ? 0.f : exp2f(m - M);
-        den = fmaf(w, __ldcg(base + r * rstride + 1), den);
+        den = fmaf(w, l, den);
       }
       // batches of 8 records: all 8 loads in flight before the accumulation (long-context
       // units have ~150 records per head)
