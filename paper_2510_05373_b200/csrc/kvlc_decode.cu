@@ -530,20 +530,24 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
         w = m == -INFINITY ? 0.f : exp2f(m - M);
         den = fmaf(w, l, den);
       }
-      // batches of 8 records: all 8 loads in flight before the accumulation (long-context
-      // units have ~150 records per head)
-      for (int i0 = 0; i0 < cnt; i0 += 8) {
-        float4 y[8];
-        float wv[8];
+      // batches of CB records: all CB loads in flight before the accumulation (long-context
+      // units have up to 52 + 2 records per head)
+#ifndef KVLC_COMBINE_BATCH
+#define KVLC_COMBINE_BATCH 8
+#endif
+      constexpr int CB = KVLC_COMBINE_BATCH;
+      for (int i0 = 0; i0 < cnt; i0 += CB) {
+        float4 y[CB];
+        float wv[CB];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < CB; ++u) {
           const int i = i0 + u;
           wv[u] = __shfl_sync(0xffffffffu, w, i & 31);
           y[u] = i < cnt ? __ldcg(reinterpret_cast<const float4*>(base + (r0 + i) * rstride + 4) + lane)
                          : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < CB; ++u) {
           const int i = i0 + u;
           if (i >= cnt) break;
           float* acc = r0 + i < a.nsq ? nr : nw;  // warp-uniform: quantized (rotated) vs residual (raw) basis
