@@ -1296,7 +1296,16 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
       return n;
     }();
     const int ws_splits = (int)std::max<int64_t>(1, (n_tok / KVLC_G + 3) / 4);  // kvlc_prefill_workspace bound
-    const int splits = std::max(1, std::min(std::min(max_nf, ws_splits), sms / (2 * units)));
+    // enough CTAs to fill whole waves (2 per unit-split: the feature halves), and at most 32
+    // chunks accumulated per TMEM partial: 63-chunk partials (an 8k sequence in a 128-unit
+    // batch) drifted to 1.3e-5 relative (T3 is 1e-5), 32-chunk ones measure 8e-6, 16-chunk
+    // ones 6e-6 but cost config 5 ~40 us in extra CTAs (tools/s_error_c2.py)
+#ifndef KVLC_TC_MAXCPC
+#define KVLC_TC_MAXCPC 32
+#endif
+    const int base = std::max({1, std::min(max_nf, sms / (2 * units)), (max_nf + KVLC_TC_MAXCPC - 1) / KVLC_TC_MAXCPC});
+    const int waves = (2 * units * base + sms - 1) / sms;  // one CTA per SM: fill the last wave
+    const int splits = std::min({ws_splits, std::max(1, max_nf), std::max(base, waves * sms / (2 * units))});
     const int cpc = (max_nf + splits - 1) / splits;
     Arena ar(ws, ws_bytes);
     float* s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
