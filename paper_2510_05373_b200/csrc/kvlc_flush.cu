@@ -709,7 +709,7 @@ struct QkSmem {
   float4 kparf[D];
 };
 #ifndef KVLC_QK_MINB
-#define KVLC_QK_MINB 2
+#define KVLC_QK_MINB 3  // 3 CTAs per SM (80 registers, 84 B spills) measured 2 % faster than 2
 #endif
 __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const FlushArgs a, const SeqInfo seq) {
   __shared__ __align__(16) QkSmem sm;
