@@ -92,6 +92,15 @@ int kvlc_ref_rotate(const double* x, int64_t rows, int64_t cols, int placement,
 int kvlc_ref_feature_map(const double* x, int64_t n, int d, const double* w1,
                          const double* w2, int h, double* out, void* stream);
 
+/* Causal attention over one head, float64 (attention.py:50-57, 99-155): q, k, v
+ * [n][d].  shifted != 0: attention_reference (max-shifted softmax; `weights`,
+ * optional, receives the [n][n] softmax rows).  shifted == 0: the corrected
+ * forms, raw exponentials plus phi_q(q_t) . phi_k(k_err_i) from phq / phk
+ * [n][rank] (NULL: no adapter): out_t = sum (e + f) v / sum (e + f). */
+int kvlc_ref_attention(const double* q, const double* k, const double* v, int64_t n,
+                       int d, const double* phq, const double* phk, int rank,
+                       int shifted, double* weights, double* out, void* stream);
+
 /* One flush of a per-head cache (cache.py:132-158): the oldest `group`
  * residual tokens k_blk/v_blk [group][d] are quantized (keys channel-wise,
  * values optionally post-rotated then token-wise) and, when w1k != NULL, the

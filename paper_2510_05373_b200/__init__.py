@@ -13,7 +13,9 @@ is `paper_2510_05373_b200.batched` / `.distributed`.
 """
 from .adapter import (CorrectionAdapter, correction_term, feature_map, phi_k, phi_q,  # noqa: F401
                       rng)
-from .attention import DecodePartial, decode_step_blocked, quantize_roundtrip  # noqa: F401
+from .attention import (DecodePartial, OpCounter, attention_reference, attention_with_config,  # noqa: F401
+                        corrected_attention_quadratic, corrected_attention_recurrent, decode_step_blocked,
+                        quantize_roundtrip)
 from .cache import (CacheFormatError, FootprintReport, KVCacheState, deserialize_cache,  # noqa: F401
                     memory_footprint, read_cache, serialize_cache, write_cache)
 from .hadamard import HadamardMatrix, hadamard_matrix, rotate  # noqa: F401
@@ -25,7 +27,8 @@ __version__ = "1.0.0"
 
 __all__ = [
     "CorrectionAdapter", "correction_term", "feature_map", "phi_q", "phi_k", "rng",
-    "DecodePartial", "decode_step_blocked", "quantize_roundtrip",
+    "DecodePartial", "decode_step_blocked", "quantize_roundtrip", "OpCounter", "attention_reference",
+    "attention_with_config", "corrected_attention_quadratic", "corrected_attention_recurrent",
     "FootprintReport", "KVCacheState", "memory_footprint", "serialize_cache", "deserialize_cache",
     "read_cache", "write_cache", "CacheFormatError",
     "HadamardMatrix", "hadamard_matrix", "rotate",

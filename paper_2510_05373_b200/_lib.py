@@ -58,6 +58,8 @@ _SIGS = {
     "kvlc_ref_rotate": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_void_p]),
     "kvlc_ref_feature_map": (c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int, c_void_p,
                                      c_void_p]),
+    "kvlc_ref_attention": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p, c_int,
+                                   c_int, c_void_p, c_void_p, c_void_p]),
     "kvlc_ref_flush_scratch": (c_size_t, [c_int, c_int, c_int]),
     "kvlc_ref_flush": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
                                c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

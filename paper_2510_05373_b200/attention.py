@@ -15,10 +15,20 @@ import numpy as np
 
 from . import _lib
 from ._device import empty_dev, to_dev, to_host
-from .adapter import CorrectionAdapter
+from .adapter import CorrectionAdapter, _feature_map_dev
 from .cache import KVCacheState
 from .hadamard import hadamard_matrix, rotate
 from .quantize import QuantConfig, quantize_tensor
+
+
+@dataclass
+class OpCounter:
+    """Counts multiply-accumulates spent on correction terms (attention.py:30-37)."""
+
+    macs: int = 0
+
+    def add(self, n: int):
+        self.macs += int(n)
 
 
 @dataclass
@@ -95,3 +105,69 @@ def quantize_roundtrip(x, cfg: QuantConfig) -> np.ndarray:
     if cfg.rotation == "post":
         return rotate(xq, h, "post")
     return xq
+
+
+# -- causal attention (prefill forms, attention.py:50-155) --------------------------
+
+def _attention_dev(q, k, v, phq, phk, rank: int, shifted: bool, want_weights: bool):
+    n, d = q.shape
+    d_out = empty_dev((n, d), "f64")
+    d_w = empty_dev((n, n), "f64") if want_weights else None
+    d_q, d_k, d_v = to_dev(q), to_dev(k), to_dev(v)  # alive until the call has been enqueued and run
+    _lib.call("kvlc_ref_attention", _lib.ptr(d_q), _lib.ptr(d_k), _lib.ptr(d_v), n, d,
+              _lib.ptr(phq), _lib.ptr(phk), rank, int(shifted), _lib.ptr(d_w), _lib.ptr(d_out), _lib.stream_handle())
+    return to_host(d_out, "f64"), (to_host(d_w, "f64") if want_weights else None)
+
+
+def attention_reference(q_mat, k_mat, v_mat):
+    """Full-precision causal attention (attention.py:50-57); returns (weights, outputs)."""
+    q, k, v = (np.asarray(x, dtype=np.float64) for x in (q_mat, k_mat, v_mat))
+    if q.shape != k.shape or k.shape != v.shape:
+        raise ValueError(f"Q/K/V shapes differ: {q.shape} {k.shape} {v.shape}")
+    out, w = _attention_dev(q, k, v, None, None, 0, shifted=True, want_weights=True)
+    return w, out
+
+
+def attention_with_config(q_mat, k_mat, v_mat, cfg_k: QuantConfig, cfg_v: QuantConfig):
+    """Causal attention over quantize-roundtripped keys and values (attention.py:91-96)."""
+    return attention_reference(q_mat, quantize_roundtrip(k_mat, cfg_k), quantize_roundtrip(v_mat, cfg_v))
+
+
+def _corrected(q_mat, k_quant, k_err, v_quant, adapter):
+    q, kq, vq = (np.asarray(x, dtype=np.float64) for x in (q_mat, k_quant, v_quant))
+    n, d = q.shape
+    use = adapter is not None and adapter.enabled
+    phq = phk = None
+    rank = 0
+    if use:
+        ke = np.asarray(k_err, dtype=np.float64)
+        w1q, w2q, w1k, w2k = adapter.device_weights()
+        h = adapter.rank // 2
+        d_q, d_ke = to_dev(q), to_dev(ke)
+        phq = _feature_map_dev(d_q, n, d, w1q, w2q, h)
+        phk = _feature_map_dev(d_ke, n, d, w1k, w2k, h)
+        rank = adapter.rank
+    out, _ = _attention_dev(q, kq, vq, phq, phk, rank, shifted=False, want_weights=False)
+    return out, use, n, d
+
+
+def corrected_attention_quadratic(q_mat, k_quant, k_err, v_quant, adapter: CorrectionAdapter | None,
+                                  counter: OpCounter | None = None):
+    """Corrected causal attention, every f(q_n, k_err_i) explicit (attention.py:99-116):
+    raw exponentials plus phi_q(q_n) . phi_k(k_err_i) over the causal prefix."""
+    out, use, n, _ = _corrected(q_mat, k_quant, k_err, v_quant, adapter)
+    if use and counter is not None:
+        counter.add(n * (n + 1) // 2 * adapter.rank)
+    return out
+
+
+def corrected_attention_recurrent(q_mat, k_quant, k_err, v_quant, adapter: CorrectionAdapter | None,
+                                  counter: OpCounter | None = None):
+    """Same outputs as the quadratic form (attention.py:119-155); the reference's running
+    (S, P) states are the prefix sums the kernel forms, and the counter charges the
+    recurrent cost (phi_k, state update, phi_q, two contractions per token)."""
+    out, use, n, d = _corrected(q_mat, k_quant, k_err, v_quant, adapter)
+    if use and counter is not None:
+        rank = adapter.rank
+        counter.add(n * (4 * d * rank + 2 * rank))
+    return out

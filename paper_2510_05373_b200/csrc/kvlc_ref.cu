@@ -226,6 +226,77 @@ __global__ void state_update_kernel(const double* __restrict__ vq, const double*
   }
 }
 
+// ------------------------------------------------------- causal attention --
+// One block per query row t over keys i <= t, float64 (attention.py:50-57, 99-155):
+//   shifted = 1: attention_reference, softmax of the masked logits (max-shifted,
+//     linalg.py:38-47); `weights` (optional) receives the [n][n] softmax rows.
+//   shifted = 0: the corrected forms, raw exponentials plus f = phi_q(q_t) . phi_k(k_err_i)
+//     (phq / phk [n][rank], NULL without adapter): out = sum (e + f) v / sum (e + f).
+// Keys are processed in tiles of blockDim: the weights of a tile go to shared memory,
+// then thread c accumulates channel c of the numerator.
+__global__ void attn_rows_kernel(const double* __restrict__ q, const double* __restrict__ k,
+                                 const double* __restrict__ v, int64_t n, int d,
+                                 const double* __restrict__ phq, const double* __restrict__ phk, int rank,
+                                 int shifted, double* __restrict__ weights, double* __restrict__ out) {
+  extern __shared__ double ash[];  // [blockDim] tile weights, [64] reduction scratch, [d] numerator
+  double* wt = ash;
+  double* red = ash + blockDim.x;
+  double* num = red + 64;
+  const int64_t t = blockIdx.x;
+  const int tid = threadIdx.x, nwarp = blockDim.x >> 5;
+  const double inv = 1.0 / sqrt((double)d);
+  const double* qt = q + t * d;
+  auto logit = [&](int64_t i) {
+    double acc = 0.0;
+    for (int c = 0; c < d; ++c) acc = fma(qt[c], k[i * d + c], acc);
+    return acc * inv;
+  };
+  double m = 0.0;
+  if (shifted) {
+    double mx = -INFINITY;
+    for (int64_t i = tid; i <= t; i += blockDim.x) mx = fmax(mx, logit(i));
+    mx = warp_max_d(mx);
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    m = red[0];
+    for (int w = 1; w < nwarp; ++w) m = fmax(m, red[w]);
+    __syncthreads();
+  }
+  for (int c = tid; c < d; c += blockDim.x) num[c] = 0.0;
+  double den = 0.0;  // per-thread partial (its keys)
+  for (int64_t i0 = 0; i0 <= t; i0 += blockDim.x) {
+    const int64_t i = i0 + tid;
+    double w = 0.0;
+    if (i <= t) {
+      w = exp(logit(i) - m);
+      if (phq) {
+        double f = 0.0;
+        for (int r = 0; r < rank; ++r) f = fma(phq[t * rank + r], phk[i * rank + r], f);
+        w += f;
+      }
+    }
+    den += w;
+    wt[tid] = w;
+    __syncthreads();
+    const int cnt = (int)(t + 1 - i0 < (int64_t)blockDim.x ? t + 1 - i0 : (int64_t)blockDim.x);
+    for (int c = tid; c < d; c += blockDim.x) {
+      double acc = num[c];
+      for (int j = 0; j < cnt; ++j) acc = fma(wt[j], v[(i0 + j) * d + c], acc);
+      num[c] = acc;
+    }
+    if (weights && i <= t) weights[t * n + i] = w;  // normalised below
+    __syncthreads();
+  }
+  den = warp_sum_d(den);
+  if ((tid & 31) == 0) red[tid >> 5] = den;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w = 0; w < nwarp; ++w) tot += red[w];
+  for (int c = tid; c < d; c += blockDim.x) out[t * d + c] = num[c] / tot;
+  if (weights)
+    for (int64_t i = tid; i < n; i += blockDim.x) weights[t * n + i] = i <= t ? weights[t * n + i] / tot : 0.0;
+}
+
 __global__ void cast_f64_f32_kernel(const double* __restrict__ q, int d, float* __restrict__ o) {
   for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = (float)q[i];
 }
@@ -504,6 +575,21 @@ int kvlc_ref_feature_map(const double* x, int64_t n, int d, const double* w1, co
   KVLC_REQUIRE(smem <= 48 * 1024, "rank %d too large for the feature-map kernel", 2 * h);
   feature_map_kernel<<<grid, 256, smem, as_stream(stream)>>>(x, n, d, w1, w2, h, out);
   return check_launch("feature_map");
+}
+
+int kvlc_ref_attention(const double* q, const double* k, const double* v, int64_t n, int d, const double* phq,
+                       const double* phk, int rank, int shifted, double* weights, double* out, void* stream) {
+  KVLC_NEED_DEVICE();
+  KVLC_REQUIRE(n >= 0 && d >= 1, "Q/K/V shapes (%lld, %d) invalid", (long long)n, d);
+  KVLC_REQUIRE(!phq == !phk && (!phq || rank >= 1), "feature matrices must come together");
+  if (n == 0) return KVLC_OK;
+  const int threads = 128;
+  const size_t smem = ((size_t)threads + 64 + d) * sizeof(double);
+  KVLC_REQUIRE(smem <= 48 * 1024, "head dim %d too large for the attention kernel", d);
+  KVLC_REQUIRE(n <= 2147483647, "sequence too long");
+  attn_rows_kernel<<<(unsigned)n, threads, smem, as_stream(stream)>>>(q, k, v, n, d, phq, phk, rank, shifted ? 1 : 0,
+                                                                     weights, out);
+  return check_launch("attention");
 }
 
 size_t kvlc_ref_flush_scratch(int d, int group, int rank) {

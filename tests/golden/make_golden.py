@@ -25,7 +25,9 @@ if REF_SRC not in sys.path:
     sys.path.insert(0, REF_SRC)
 
 from quantkv.adapter import CorrectionAdapter, feature_map, phi_k, phi_q  # noqa: E402
-from quantkv.attention import decode_step_blocked  # noqa: E402
+from quantkv.attention import (OpCounter, attention_reference,  # noqa: E402
+                               corrected_attention_quadratic, corrected_attention_recurrent,
+                               decode_step_blocked)
 from quantkv.cache import KVCacheState, memory_footprint, serialize_cache  # noqa: E402
 from quantkv.hadamard import hadamard_matrix, rotate  # noqa: E402
 from quantkv.linalg import rng  # noqa: E402
@@ -210,9 +212,41 @@ def cache_cases():
     return out
 
 
+ATTN_CASES = [  # name, seed, n, d, rank (0 = no adapter), adapter seed
+    ("a_small", 0, 24, 8, 8, 3),
+    ("a_noad", 1, 40, 16, 0, 0),
+    ("a_mid", 2, 96, 32, 16, 7),
+    ("a_prod", 3, 300, 128, 256, 0),
+]
+
+
+def attention_cases():
+    """Causal prefill attention (attention.py:50-155) on quantized inputs built like the
+    reference tests' quantized_inputs (test_attention.py:145-154)."""
+    out = {}
+    for name, seed, n, d, rank, aseed in ATTN_CASES:
+        g = rng(seed)
+        q = g.standard_normal((n, d))
+        k = g.standard_normal((n, d))
+        v = g.standard_normal((n, d))
+        k_hat = quantize_tensor(k, QuantConfig(bits=2, group_size=n, axis="channel")).dequantize()
+        v_hat = quantize_tensor(v, QuantConfig(bits=2, group_size=d, axis="token")).dequantize()
+        ad = CorrectionAdapter.initialize(d, rank, seed=aseed) if rank else None
+        p = f"{name}/"
+        out[p + "meta"] = np.array([seed, n, d, rank, aseed])
+        out[p + "q"], out[p + "k_hat"], out[p + "k_err"], out[p + "v_hat"] = q, k_hat, k - k_hat, v_hat
+        w, y = attention_reference(q, k_hat, v_hat)
+        out[p + "ref_w"], out[p + "ref_y"] = w, y
+        cq, cr = OpCounter(), OpCounter()
+        out[p + "quad"] = corrected_attention_quadratic(q, k_hat, k - k_hat, v_hat, ad, cq)
+        out[p + "rec"] = corrected_attention_recurrent(q, k_hat, k - k_hat, v_hat, ad, cr)
+        out[p + "macs"] = np.array([cq.macs, cr.macs])
+    return out
+
+
 def main():
     for fname, fn in (("quantize", quantize_cases), ("hadamard", hadamard_cases),
-                      ("adapter", adapter_cases), ("cache", cache_cases)):
+                      ("adapter", adapter_cases), ("cache", cache_cases), ("attention", attention_cases)):
         data = fn()
         path = os.path.join(HERE, f"{fname}.npz")
         np.savez_compressed(path, **data)

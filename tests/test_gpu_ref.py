@@ -288,3 +288,47 @@ def test_quantize_roundtrip_matches_reference_composition(rotation, bits, shape)
     xq = xr if bits == 16 else orc.dequantize_matrix(orc.quantize_matrix(xr, bits, 16, axis))
     want = h.T @ xq if rotation == "pre" else (xq @ h.T if rotation == "post" else xq)
     assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+def test_prefill_attention_forms_match_reference(golden):
+    """attention_reference, attention_with_config and the corrected quadratic / recurrent
+    forms (attention.py:50-155) against the reference's outputs, with its MAC counters."""
+    z = golden["attention"]
+    for name in sorted({k.split("/")[0] for k in z if k.endswith("/meta")}):
+        seed, n, d, rank, aseed = (int(x) for x in z[f"{name}/meta"])
+        q, kq, ke, vq = (z[f"{name}/{x}"] for x in ("q", "k_hat", "k_err", "v_hat"))
+        w, y = qk.attention_reference(q, kq, vq)
+        assert np.max(np.abs(w - z[f"{name}/ref_w"])) <= 1e-13, name
+        assert np.max(np.abs(y - z[f"{name}/ref_y"])) <= 1e-12, name
+        ad = qk.CorrectionAdapter.initialize(d, rank, seed=aseed) if rank else None
+        cq, cr = qk.OpCounter(), qk.OpCounter()
+        quad = qk.corrected_attention_quadratic(q, kq, ke, vq, ad, cq)
+        rec = qk.corrected_attention_recurrent(q, kq, ke, vq, ad, cr)
+        assert np.max(np.abs(quad - z[f"{name}/quad"])) <= 1e-12, name
+        assert np.max(np.abs(rec - z[f"{name}/rec"])) <= 1e-10, name
+        assert [cq.macs, cr.macs] == list(z[f"{name}/macs"]), name
+
+
+def test_prefill_attention_reference_properties():
+    """The reference's own checks (test_attention.py:157-205): no adapter == plain
+    attention, k_err = 0 closed form, first recurrent output = first value, shapes."""
+    from oracle import kvlinc_oracle as orc
+    g = orc.rng(0)
+    n, d = 24, 8
+    q, k, v = (g.standard_normal((n, d)) for _ in range(3))
+    _, want = qk.attention_reference(q, k, v)
+    for ad in (None, qk.CorrectionAdapter.initialize(8, 8, enabled=False)):
+        assert np.max(np.abs(qk.corrected_attention_quadratic(q, k, k * 0, v, ad) - want)) <= 1e-12
+    ad = qk.CorrectionAdapter.initialize(8, 16, seed=5)
+    got = qk.corrected_attention_quadratic(q, k, np.zeros_like(k), v, ad)
+    mask = np.arange(n)[None, :] <= np.arange(n)[:, None]
+    e = np.where(mask, np.exp(q @ k.T / np.sqrt(8)), 0.0) + mask * (4.0 / 16.0)
+    assert np.max(np.abs(got - (e @ v) / e.sum(axis=1, keepdims=True))) <= 1e-12
+    rec = qk.corrected_attention_recurrent(q[:1], k[:1], k[:1] * 0.1, v[:1], ad)
+    assert np.max(np.abs(rec[0] - v[0])) <= 1e-12
+    cfg = qk.QuantConfig(bits=2, group_size=8, axis="token", rotation="post")
+    a_cfg, y_cfg = qk.attention_with_config(q, k, v, cfg, cfg)
+    a_ref, y_ref = qk.attention_reference(q, qk.quantize_roundtrip(k, cfg), qk.quantize_roundtrip(v, cfg))
+    assert np.array_equal(a_cfg, a_ref) and np.array_equal(y_cfg, y_ref)
+    with pytest.raises(ValueError, match="Q/K/V shapes differ"):
+        qk.attention_reference(q, k[:3], v)

@@ -157,3 +157,18 @@ def test_serialization_matches_reference(golden):
         ref = z[f"{name}/kvlc"].tobytes()
         assert orc.serialize(c) == ref, name
         assert orc.serialize(orc.deserialize(ref)) == ref, name
+
+
+def test_prefill_attention_matches_reference(golden):
+    """attention_reference and the corrected quadratic / recurrent forms (attention.py:50-155)."""
+    z = golden["attention"]
+    for name in sorted({k.split("/")[0] for k in z if k.endswith("/meta")}):
+        seed, n, d, rank, aseed = (int(x) for x in z[f"{name}/meta"])
+        q, kq, ke, vq = (z[f"{name}/{x}"] for x in ("q", "k_hat", "k_err", "v_hat"))
+        w, y = orc.attention_reference(q, kq, vq)
+        assert np.max(np.abs(w - z[f"{name}/ref_w"])) <= 1e-13, name
+        assert np.max(np.abs(y - z[f"{name}/ref_y"])) <= 1e-12, name
+        ad = orc.init_adapter(d, rank, seed=aseed) if rank else None
+        c = orc.corrected_attention(q, kq, ke, vq, ad)
+        assert np.max(np.abs(c - z[f"{name}/quad"])) <= 1e-12, name
+        assert np.max(np.abs(c - z[f"{name}/rec"])) <= 1e-10, name
