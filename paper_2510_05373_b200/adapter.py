@@ -3,7 +3,8 @@
 `CorrectionAdapter` holds the four (d, D/2) weights exactly like the
 reference (same PCG64 initialisation, adapter.py:67-77); the feature map
 phi(x) = [softmax(x W1), softmax(x W2)] runs in the `kvlc_ref_feature_map`
-kernel (float64).  Adapter training (adapter.py:104-362) is out of scope.
+kernel (float64).  Adapter training and the .kvla format (adapter.py:104-362) are in
+`train.py`.
 """
 from __future__ import annotations
 

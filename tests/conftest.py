@@ -19,7 +19,7 @@ def pytest_configure(config):
 def golden():
     """Golden vectors produced by running the reference (tests/golden/make_golden.py)."""
     out = {}
-    for name in ("quantize", "hadamard", "adapter", "cache", "attention"):
+    for name in ("quantize", "hadamard", "adapter", "cache", "attention", "train"):
         with np.load(os.path.join(GOLDEN, f"{name}.npz")) as z:
             out[name] = {k: z[k] for k in z.files}
     return out

@@ -24,7 +24,9 @@ REF_SRC = "/root/reference/pkg/src"
 if REF_SRC not in sys.path:
     sys.path.insert(0, REF_SRC)
 
-from quantkv.adapter import CorrectionAdapter, feature_map, phi_k, phi_q  # noqa: E402
+from quantkv.adapter import (CorrectionAdapter, TrainSettings, _batched_loss_and_grads,  # noqa: E402
+                             corrected_weights, feature_map, loss_and_grads, phi_k, phi_q,
+                             serialize_adapter, train_adapter)
 from quantkv.attention import (OpCounter, attention_reference,  # noqa: E402
                                corrected_attention_quadratic, corrected_attention_recurrent,
                                decode_step_blocked)
@@ -244,9 +246,43 @@ def attention_cases():
     return out
 
 
+def train_cases():
+    """Adapter calibration (adapter.py:104-307): corrected rows, per-item and batched
+    loss / gradients, a short Adam run, the .kvla bytes."""
+    out = {}
+    g = rng(90)
+    n, d, rank = 48, 16, 8
+    q = g.standard_normal((n, d))
+    k = g.standard_normal((n, d))
+    v = g.standard_normal((n, d))
+    k_hat = quantize_tensor(k, QuantConfig(bits=2, group_size=16, axis="channel")).dequantize()
+    k_err = k - k_hat
+    ad = CorrectionAdapter.initialize(d, rank, seed=4)
+    a_full, _ = attention_reference(q, k, v)
+    out["t/q"], out["t/k"], out["t/v"], out["t/k_hat"] = q, k, v, k_hat
+    out["t/cw"] = corrected_weights(q[10], k_hat[:11], k_err[:11], ad)
+    batch = [(a_full[t, : t + 1], q[t], k_hat[: t + 1], k_err[: t + 1]) for t in (3, 17, 40)]
+    loss, grads = loss_and_grads(batch, ad)
+    out["t/item_loss"] = np.array([loss])
+    for name, gr in grads.items():
+        out[f"t/item_{name}"] = gr
+    pos = np.array([2, 9, 30, 47])
+    loss, grads = _batched_loss_and_grads(a_full, pos, q, k_hat, k_err, ad)
+    out["t/batch_loss"] = np.array([loss])
+    for name, gr in grads.items():
+        out[f"t/batch_{name}"] = gr
+    trained, losses = train_adapter(q, k, v, TrainSettings(rank=rank, steps=6, lr=0.05, batch=16, seed=2,
+                                                           group_size=16))
+    out["t/losses"] = np.asarray(losses)
+    for name in ("w1_q", "w2_q", "w1_k", "w2_k"):
+        out[f"t/trained_{name}"] = getattr(trained, name)
+    out["t/kvla"] = np.frombuffer(serialize_adapter(ad), np.uint8)
+    return out
+
+
 def main():
     for fname, fn in (("quantize", quantize_cases), ("hadamard", hadamard_cases),
-                      ("adapter", adapter_cases), ("cache", cache_cases), ("attention", attention_cases)):
+                      ("adapter", adapter_cases), ("cache", cache_cases), ("attention", attention_cases), ("train", train_cases)):
         data = fn()
         path = os.path.join(HERE, f"{fname}.npz")
         np.savez_compressed(path, **data)

@@ -332,3 +332,34 @@ def test_prefill_attention_reference_properties():
     assert np.array_equal(a_cfg, a_ref) and np.array_equal(y_cfg, y_ref)
     with pytest.raises(ValueError, match="Q/K/V shapes differ"):
         qk.attention_reference(q, k[:3], v)
+
+
+def test_adapter_training_matches_reference(golden):
+    """Adapter calibration (adapter.py:104-307) against the reference's outputs: corrected
+    rows, per-item and batched loss / gradients, a 6-step Adam run."""
+    from paper_2510_05373_b200 import train as tr
+    z = golden["train"]
+    q, k, v, k_hat = z["t/q"], z["t/k"], z["t/v"], z["t/k_hat"]
+    k_err = k - k_hat
+    n, d = q.shape
+    ad = qk.CorrectionAdapter.initialize(d, 8, seed=4)
+    assert np.max(np.abs(qk.corrected_weights(q[10], k_hat[:11], k_err[:11], ad) - z["t/cw"])) <= 1e-14
+    a_full, _ = qk.attention_reference(q, k, v)
+    batch = [(a_full[t, : t + 1], q[t], k_hat[: t + 1], k_err[: t + 1]) for t in (3, 17, 40)]
+    loss, grads = qk.loss_and_grads(batch, ad)
+    assert abs(loss - z["t/item_loss"][0]) <= 1e-12
+    for name, g in grads.items():
+        assert np.max(np.abs(g - z[f"t/item_{name}"])) <= 1e-12 * max(1.0, np.abs(z[f"t/item_{name}"]).max()), name
+    loss, grads = tr._batched_loss_and_grads(a_full, np.array([2, 9, 30, 47]), q, k_hat, k_err, ad)
+    assert abs(loss - z["t/batch_loss"][0]) <= 1e-12
+    for name, g in grads.items():
+        assert np.max(np.abs(g - z[f"t/batch_{name}"])) <= 1e-12 * max(1.0, np.abs(z[f"t/batch_{name}"]).max()), name
+    trained, losses = qk.train_adapter(q, k, v, qk.TrainSettings(rank=8, steps=6, lr=0.05, batch=16, seed=2,
+                                                                 group_size=16))
+    assert np.max(np.abs(np.asarray(losses) - z["t/losses"])) <= 1e-10
+    for name in ("w1_q", "w2_q", "w1_k", "w2_k"):
+        assert np.max(np.abs(getattr(trained, name) - z[f"t/trained_{name}"])) <= 1e-10, name
+    with pytest.raises(ValueError, match="non-empty"):
+        qk.loss_and_grads([], ad)
+    zero = qk.train_adapter(q, k, v, qk.TrainSettings(rank=8, steps=0, seed=2, group_size=16))[0]
+    assert np.array_equal(zero.w1_q, qk.CorrectionAdapter.initialize(d, 8, seed=2).w1_q)

@@ -145,3 +145,23 @@ def test_kvlc_format_round_trips_reference_bytes(golden):
     with pytest.raises(fmt.CacheFormatError, match="trailing bytes at byte"):
         fmt.split(ref + b"\0", h)
     assert issubclass(fmt.CacheFormatError, ValueError)
+
+
+def test_adapter_file_format_matches_reference(golden, tmp_path):
+    """.kvla bytes (adapter.py:310-362): host-side format, byte-identical to the reference."""
+    import pytest
+    from paper_2510_05373_b200 import CorrectionAdapter, train
+    want = golden["train"]["t/kvla"].tobytes()
+    ad = CorrectionAdapter.initialize(16, 8, seed=4)
+    assert train.serialize_adapter(ad) == want
+    back = train.deserialize_adapter(want)
+    assert train.serialize_adapter(back) == want and back.enabled
+    path = tmp_path / "a.kvla"
+    train.write_adapter(ad, path)
+    assert train.read_adapter(path).rank == 8
+    with pytest.raises(train.AdapterFormatError, match="bad magic"):
+        train.deserialize_adapter(b"XXXX" + want[4:])
+    with pytest.raises(train.AdapterFormatError, match="payload size mismatch"):
+        train.deserialize_adapter(want[:-4])
+    with pytest.raises(train.AdapterFormatError, match="too short"):
+        train.deserialize_adapter(want[:8])
