@@ -19,6 +19,7 @@ from .attention import (DecodePartial, OpCounter, attention_reference, attention
 from .cache import (CacheFormatError, FootprintReport, KVCacheState, deserialize_cache,  # noqa: F401
                     memory_footprint, read_cache, serialize_cache, write_cache)
 from .hadamard import HadamardMatrix, hadamard_matrix, rotate  # noqa: F401
+from .linalg import matmul, softmax_rows  # noqa: F401
 from .train import (AdamState, AdapterFormatError, TrainSettings, corrected_weights,  # noqa: F401
                     deserialize_adapter, loss_and_grads, read_adapter, serialize_adapter, train_adapter,
                     write_adapter)
@@ -34,7 +35,7 @@ __all__ = [
     "attention_with_config", "corrected_attention_quadratic", "corrected_attention_recurrent",
     "FootprintReport", "KVCacheState", "memory_footprint", "serialize_cache", "deserialize_cache",
     "read_cache", "write_cache", "CacheFormatError",
-    "HadamardMatrix", "hadamard_matrix", "rotate",
+    "HadamardMatrix", "hadamard_matrix", "rotate", "matmul", "softmax_rows",
     "AdamState", "AdapterFormatError", "TrainSettings", "corrected_weights", "loss_and_grads", "train_adapter",
     "serialize_adapter", "deserialize_adapter", "read_adapter", "write_adapter",
     "QuantConfig", "QuantizedTensor", "dequantize_group", "expected_quant_mse", "pack_codes",

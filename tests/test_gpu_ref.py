@@ -363,3 +363,21 @@ def test_adapter_training_matches_reference(golden):
         qk.loss_and_grads([], ad)
     zero = qk.train_adapter(q, k, v, qk.TrainSettings(rank=8, steps=0, seed=2, group_size=16))[0]
     assert np.array_equal(zero.w1_q, qk.CorrectionAdapter.initialize(d, 8, seed=2).w1_q)
+
+
+def test_linalg_substrate():
+    """matmul / softmax_rows (linalg.py:28-47) with the reference's messages."""
+    from oracle import kvlinc_oracle as orc
+    g = orc.rng(3)
+    a, b = g.standard_normal((5, 7)), g.standard_normal((7, 3))
+    assert np.max(np.abs(qk.matmul(a, b) - a @ b)) <= 1e-13
+    x = g.standard_normal((4, 6))
+    x[1, 2:] = -np.inf
+    s = qk.softmax_rows(x)
+    want = np.exp(x - x.max(axis=1, keepdims=True))
+    want /= want.sum(axis=1, keepdims=True)
+    assert np.max(np.abs(s - want)) <= 1e-15 and np.all(s[1, 2:] == 0)
+    with pytest.raises(ValueError, match="inner dims differ"):
+        qk.matmul(a, a)
+    with pytest.raises(ValueError, match="2-D operands"):
+        qk.matmul(a[0], b)
