@@ -89,7 +89,8 @@ def oracle_decode(q, ocs, adapters, literal=False):
 
 
 @pytest.mark.parametrize("Hkv,Hq,lens", [(2, 8, [900, 511]), (1, 7, [640]), (2, 2, [300, 1000]),
-                                         (1, 8, [385])])
+                                         (1, 8, [385]), (2, 4, [700, 257]), (1, 3, [520, 129, 1]),
+                                         (2, 10, [600]), (1, 6, [1100, 384])])
 def test_prefill_and_decode_vs_oracle(Hkv, Hq, lens):
     B = len(lens)
     n = max(lens)
