@@ -34,7 +34,6 @@ namespace kvlc {
 namespace {
 
 constexpr int D = KVLC_D;
-constexpr int G = KVLC_G;
 constexpr int SLOTS = KVLC_SLOTS;
 constexpr int RANK = KVLC_RANK;
 constexpr int HALF = RANK / 2;
@@ -42,7 +41,6 @@ constexpr int WARPS = 4;
 constexpr int THREADS = WARPS * 32;
 constexpr int REC = 4 + D;  // record: m (log2 units), l, pad, pad, y[D] (16-byte aligned y)
 constexpr int PREC = 4 + 2 * D;  // device-partial record: m, l, pad, pad, y_rot[D], y_raw[D]
-constexpr float LOG2E = 1.4426950408889634f;
 constexpr float C0 = 0.12751743074173226f;  // log2(e) / sqrt(128)
 
 __device__ __forceinline__ float bf2f(uint16_t x) { return __uint_as_float((uint32_t)x << 16); }
@@ -79,14 +77,6 @@ __device__ __forceinline__ uint4 ldg4(const void* p) {
 }
 __device__ __forceinline__ uint2 ldg2(const void* p) {
   return __ldg(reinterpret_cast<const uint2*>(p));
-}
-__device__ __forceinline__ uint32_t w4(const uint4& v, int i) {
-  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
-}
-
-// byte b of x into byte 0 and byte b of y into byte 2 (bytes 1, 3 are masked off later)
-__device__ __forceinline__ uint32_t pick(uint32_t x, uint32_t y, int b) {
-  return __byte_perm(x, y, (uint32_t)(b | (b << 4) | ((4 + b) << 8) | ((4 + b) << 12)));
 }
 // half2 of fp16 subnormals (c_lo * 4^j * 2^-24, c_hi * 4^j * 2^-24)
 __device__ __forceinline__ uint32_t code_h2(uint32_t x, int j) { return x & (0x00030003u << (2 * j)); }
@@ -813,7 +803,7 @@ using namespace kvlc;
 extern "C" {
 
 size_t kvlc_decode_workspace(const kvlc_cache* c, const kvlc_decode_opts* o) {
-  Plan p;
+  Plan p{};
   if (!c || plan_for(c, o, 0, 1 << 30, 1, true, p)) return 0;
   return p.total;
 }
@@ -822,7 +812,7 @@ int kvlc_decode(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, 
                 const kvlc_decode_opts* o, void* ws, size_t ws_bytes, void* stream) {
   KVLC_NEED_DEVICE();
   KVLC_REQUIRE(q && out, "null query / output");
-  Plan p;
+  Plan p{};
   int rc = plan_for(c, o, 0, 1 << 30, 1, adapter_active(ad), p);
   if (rc) return rc;
   KVLC_REQUIRE(ws && ws_bytes >= p.total, "decode workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
@@ -838,7 +828,7 @@ int kvlc_decode_partial(const kvlc_cache* c, const kvlc_adapter* ad, const uint1
   KVLC_REQUIRE(q && rec, "null query / record buffer");
   KVLC_REQUIRE(chunk_lo >= 0 && chunk_hi >= chunk_lo, "bad chunk window [%d, %d)", chunk_lo, chunk_hi);
   KVLC_REQUIRE(!include_tail || !adapter_active(ad) || corr, "tail owner needs a correction buffer");
-  Plan p;
+  Plan p{};
   int rc = plan_for(c, o, chunk_lo, chunk_hi, include_tail ? 1 : 0, adapter_active(ad), p);
   if (rc) return rc;
   KVLC_REQUIRE(ws && ws_bytes >= p.total, "decode workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
