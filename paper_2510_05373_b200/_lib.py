@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_float, c_int, c_int32, c_int64, c_size_t, c_uint16, c_uint32, c_void_p
+from ctypes import POINTER, c_int, c_int32, c_int64, c_size_t, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KVLC_LIB") or os.path.join(_HERE, "libkvlinc.so")  # KVLC_LIB: tracing build

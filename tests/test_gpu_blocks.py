@@ -6,7 +6,6 @@ float64 oracle value rounded once to fp32.  kvlc_state_update: S, P within
 1e-6 relative of the float64 loop (cache.py:155-158).  kvlc_flush_due: a deferred
 flush leaves the cache byte-identical to the streaming append rule.
 """
-import ctypes
 
 import numpy as np
 import pytest
