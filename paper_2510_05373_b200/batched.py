@@ -276,6 +276,41 @@ class BatchedKVCache:
             self.decode(q, adapters, literal, out, chunks_per_split)
         return graph, out
 
+    def steps_until_flush(self) -> int:
+        """Appends every sequence can take before one of them reaches R + G (flushes)."""
+        return int(np.min(R + G - 1 - self.res_len))
+
+    def capture_serving_step(self, q: torch.Tensor, k_t: torch.Tensor, v_t: torch.Tensor,
+                             adapters: AdapterBank | None = None, out: torch.Tensor | None = None):
+        """One steady-state decode-loop step in one CUDA graph: append k_t, v_t (one token
+        per sequence, cache.py:120-130) then the fused decode of q.  Refill q / k_t / v_t
+        in place and call `.replay()`; each replay advances the host length mirrors and
+        refuses to run into a flush (run that step eagerly: `append` then `decode`)."""
+        if k_t.shape != (self.B, self.Hkv, D) or v_t.shape != k_t.shape:
+            raise ValueError(f"token dims {tuple(k_t.shape)}/{tuple(v_t.shape)} != ({self.B}, {self.Hkv}, {D})")
+        if out is None:
+            out = torch.empty(q.shape, dtype=torch.bfloat16, device=self.device)
+        self.decode(q, adapters, out=out)  # sizes the decode workspace
+        torch.cuda.synchronize()
+        ad = _adapter_struct(adapters)
+        a_c = (ctypes.c_int32 * self.B)(*([1] * self.B))
+        f_c = (ctypes.c_int32 * self.B)(*([0] * self.B))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            _lib.call("kvlc_append", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
+                      a_c, f_c, None, 0, _lib.stream_handle())
+            self.decode(q, adapters, out=out)
+        cache = self
+
+        class _Step:
+            def replay(self):
+                if cache.steps_until_flush() < 1:
+                    raise ValueError("a sequence flushes on this append: run the step eagerly")
+                graph.replay()
+                cache.res_len = cache.res_len + 1
+
+        return _Step(), out
+
     def decode_partial(self, q: torch.Tensor, chunk_lo: int, chunk_hi: int, include_tail: bool,
                        adapters: AdapterBank | None = None, chunks_per_split: int = 0,
                        rec: torch.Tensor | None = None, corr: torch.Tensor | None = None):

@@ -246,3 +246,34 @@ def test_host_output_graph_matches_device_output():
     assert torch.equal(out_host, want)
     with pytest.raises(ValueError, match="pinned"):
         cache.decode(tdev(q), adapters=bank, out=torch.empty((B, Hq, D), dtype=torch.bfloat16))
+
+
+def test_serving_step_graph_equals_eager_steps():
+    """capture_serving_step: append + decode replayed from one graph == the eager calls,
+    step by step, up to the flush boundary (which it refuses)."""
+    B, Hkv, Hq = 2, 2, 8
+    g = orc.rng(21)
+    n0 = 300
+    k = tdev(bf16_round(g.standard_normal((B, Hkv, n0, D)).astype(np.float32)))
+    bank = AdapterBank.initialize(Hkv)
+    a = BatchedKVCache(B, Hkv, Hq, max_tokens=1024)
+    b = BatchedKVCache(B, Hkv, Hq, max_tokens=1024)
+    a.prefill(k, k, adapters=bank)
+    b.prefill(k, k, adapters=bank)
+    q = torch.empty((B, Hq, D), dtype=torch.bfloat16, device="cuda")
+    kt = torch.empty((B, Hkv, D), dtype=torch.bfloat16, device="cuda")
+    vt = torch.empty_like(kt)
+    step, out = a.capture_serving_step(q, kt, vt, adapters=bank)
+    n_steps = a.steps_until_flush()
+    assert n_steps == 255 - (n0 - 128)
+    for i in range(n_steps):
+        q.copy_(tdev(g.standard_normal((B, Hq, D))))
+        kt.copy_(tdev(g.standard_normal((B, Hkv, D))))
+        vt.copy_(tdev(g.standard_normal((B, Hkv, D))))
+        step.replay()
+        b.append(kt, vt, adapters=bank)
+        want = b.decode(q, adapters=bank)
+        assert torch.equal(out, want), i
+    assert np.array_equal(a.res_len, b.res_len)
+    with pytest.raises(ValueError, match="eagerly"):
+        step.replay()
