@@ -201,6 +201,10 @@ int kvlc_prefill(const kvlc_cache* cache, const kvlc_adapter* ad,
                  size_t ws_bytes, void* stream);
 size_t kvlc_prefill_workspace(const kvlc_cache* cache, int64_t n_tok);
 
+/* Workspace for kvlc_append / kvlc_flush_due to run their flushes on the tensor-core path
+ * (with an adapter); without it (ws NULL or smaller) they use the SIMT flush kernel. */
+size_t kvlc_append_workspace(const kvlc_cache* cache);
+
 /* Append one token per sequence (cache.py:120-130): k_t, v_t bf16
  * [B][Hkv][128].  active_host[b] != 0 selects the sequences that append;
  * flush_host[b] != 0 flushes sequence b's oldest G tokens afterwards (the

@@ -72,6 +72,7 @@ _SIGS = {
     "kvlc_prefill_workspace": (c_size_t, [POINTER(KvlcCache), c_int64]),
     "kvlc_prefill": (c_int, [POINTER(KvlcCache), POINTER(KvlcAdapter), c_void_p, c_void_p, c_int64,
                              POINTER(c_int32), c_int32, c_void_p, c_size_t, c_void_p]),
+    "kvlc_append_workspace": (c_size_t, [POINTER(KvlcCache)]),
     "kvlc_append": (c_int, [POINTER(KvlcCache), POINTER(KvlcAdapter), c_void_p, c_void_p,
                             POINTER(c_int32), POINTER(c_int32), c_void_p, c_size_t, c_void_p]),
     "kvlc_decode_workspace": (c_size_t, [POINTER(KvlcCache), POINTER(KvlcDecodeOpts)]),

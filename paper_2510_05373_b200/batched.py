@@ -134,6 +134,13 @@ class BatchedKVCache:
                          p(self.vres), p(self.S), p(self.P), p(self.n_chunks_dev),
                          p(self.res_start_dev), p(self.res_len_dev))
 
+    def _flush_ws(self, flush, adapters):
+        """(pointer, bytes) of the tensor-core flush workspace when an adapter flush is due."""
+        if not np.any(flush) or not _adapters_on(adapters):
+            return None, 0
+        ws = self.workspace(_lib.load().kvlc_append_workspace(ctypes.byref(self._struct)))
+        return _ptr(ws), ws.numel()
+
     def workspace(self, nbytes: int) -> torch.Tensor:
         """Scratch for prefill / append (contents are transient)."""
         if self._ws is None or self._ws.numel() < nbytes:
@@ -206,8 +213,9 @@ class BatchedKVCache:
         f_c = (ctypes.c_int32 * self.B)(*flush.astype(np.int32).tolist())
         k_t = k_t.to(self.device, torch.bfloat16).contiguous()
         v_t = v_t.to(self.device, torch.bfloat16).contiguous()
+        ws, nws = self._flush_ws(flush, adapters)
         _lib.call("kvlc_append", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
-                  a_c, f_c, None, 0, _lib.stream_handle())
+                  a_c, f_c, ws, nws, _lib.stream_handle())
         if _adapters_on(adapters):
             self.state_rank[flush] = RANK
         self.res_len = new_len - flush * G
@@ -343,8 +351,9 @@ class BatchedKVCache:
         if np.any(self.n_chunks + flush > self.max_chunks):
             raise ValueError(f"flush exceeds capacity of {self.max_tokens} tokens")
         f_c = (ctypes.c_int32 * self.B)(*flush.astype(np.int32).tolist())
+        ws, nws = self._flush_ws(flush, adapters)
         _lib.call("kvlc_flush_due", ctypes.byref(self._struct), ctypes.byref(_adapter_struct(adapters)), f_c,
-                  None, 0, _lib.stream_handle())
+                  ws, nws, _lib.stream_handle())
         if _adapters_on(adapters):
             self.state_rank[flush] = RANK
         self.res_len = self.res_len - flush * G

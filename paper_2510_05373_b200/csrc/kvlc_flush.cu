@@ -719,10 +719,19 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
   if (ci >= seq.nflush[b]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool writer = true;
-  const int64_t tok0 = (int64_t)ci * G;
+  // prefill: chunk ci of the sequence's tokens; ring (decode-time flush): the oldest G slots of
+  // the residual ring into the sequence's next chunk (cache.py:132-147)
+  const int64_t tok0 = a.ring ? (int64_t)c.res_start[b] + (int64_t)ci * G : (int64_t)ci * G;
   const uint16_t* K = a.ksrc + unit * a.k_unit + tok0 * a.k_t;
   const uint16_t* V = a.vsrc + unit * a.v_unit + tok0 * a.v_t;
-  const size_t cb = (size_t)unit * c.max_chunks + ci;
+  const size_t cb = (size_t)unit * c.max_chunks + (a.ring ? c.n_chunks[b] + ci : ci);
+  // 4 channels 4 lane .. 4 lane + 3 of value row t (contiguous, or the ring's channel-major layout)
+  auto ldv = [&](int t) -> uint2 {
+    if (a.v_c == 1) return __ldg(reinterpret_cast<const uint2*>(V + (size_t)t * a.v_t + lane * 4));
+    const uint16_t* p = V + (size_t)t * a.v_t + (size_t)(lane * 4) * a.v_c;
+    return make_uint2((uint32_t)__ldg(p) | ((uint32_t)__ldg(p + a.v_c) << 16),
+                      (uint32_t)__ldg(p + 2 * a.v_c) | ((uint32_t)__ldg(p + 3 * a.v_c) << 16));
+  };
   const size_t slot = (size_t)unit * a.slot_stride + ci;
     // ---- K1: keys, channel-wise.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3
     // (16-B vector loads).  Codes in fp32 with the exact fp64 decision near rounding
@@ -825,7 +834,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
     uint2 vpf[VPF];
 #pragma unroll
     for (int i = 0; i < VPF; ++i)
-      vpf[i] = __ldg(reinterpret_cast<const uint2*>(V + (size_t)(warp + 8 * i) * a.v_t + lane * 4));
+      vpf[i] = ldv(warp + 8 * i);
 #pragma unroll 1
     for (int ti = 0; ti < VTOK; ++ti) {
       const int t = warp + 8 * ti;
@@ -835,7 +844,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
 #pragma unroll
         for (int i = 0; i < VPF - 1; ++i) vpf[i] = vpf[i + 1];
         if (ti + VPF < VTOK)
-          vpf[VPF - 1] = __ldg(reinterpret_cast<const uint2*>(V + (size_t)(t + 8 * VPF) * a.v_t + lane * 4));
+          vpf[VPF - 1] = ldv(t + 8 * VPF);
         xf[0] = __uint_as_float(raw.x << 16);
         xf[1] = __uint_as_float(raw.x & 0xffff0000u);
         xf[2] = __uint_as_float(raw.y << 16);
@@ -891,7 +900,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         const double hs = 1.0 / sqrt((double)D);
         double x[4], y[4];
         {
-          const uint2 raw = __ldg(reinterpret_cast<const uint2*>(V + (size_t)t * a.v_t + lane * 4));
+          const uint2 raw = ldv(t);
           y[0] = (double)__uint_as_float(raw.x << 16);
           y[1] = (double)__uint_as_float(raw.x & 0xffff0000u);
           y[2] = (double)__uint_as_float(raw.y << 16);
@@ -1227,6 +1236,62 @@ int kvlc_ftrace_copy(void* dst, size_t bytes) {
 }
 namespace {
 #endif
+// The tensor-core flush (quant_kernel -> flush_tc_kernel -> reduce_state) of the chunks
+// seq.nflush[b] per sequence; `a` carries the source (prefill tokens or the ring).  The
+// workspace is kvlc_prefill_workspace(c, n_tok) bytes.
+int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, const SeqInfo& seq, int max_nf,
+                    int64_t n_tok, void* ws, size_t ws_bytes, cudaStream_t s) {
+  int rc = 0;
+  const int units = c->B * c->Hkv;
+  static int sms = [] {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  const int ws_splits = (int)std::max<int64_t>(1, (n_tok / KVLC_G + 3) / 4);  // kvlc_prefill_workspace bound
+  // enough CTAs to fill whole waves (2 per unit-split: the feature halves), and at most 32
+  // chunks accumulated per TMEM partial: 63-chunk partials (an 8k sequence in a 128-unit
+  // batch) drifted to 1.3e-5 relative (T3 is 1e-5), 32-chunk ones measure 8e-6, 16-chunk
+  // ones 6e-6 but cost config 5 ~40 us in extra CTAs (tools/s_error_c2.py)
+#ifndef KVLC_TC_MAXCPC
+#define KVLC_TC_MAXCPC 32
+#endif
+  const int base = std::max({1, std::min(max_nf, sms / (2 * units)), (max_nf + KVLC_TC_MAXCPC - 1) / KVLC_TC_MAXCPC});
+  const int waves = (2 * units * base + sms - 1) / sms;  // one CTA per SM: fill the last wave
+  const int splits = std::min({ws_splits, std::max(1, max_nf), std::max(base, waves * sms / (2 * units))});
+  const int cpc = (max_nf + splits - 1) / splits;
+  Arena ar(ws, ws_bytes);
+  float* s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
+  uint8_t* wtiles = ar.take<uint8_t>((size_t)c->Hkv * 2 * 2 * FT_TILE);
+  const int slot_stride = (int)std::max<int64_t>(1, n_tok / KVLC_G);
+  uint8_t* aimg = ar.take<uint8_t>((size_t)units * slot_stride * 2 * FT_TILE);
+  uint8_t* cimg = ar.take<uint8_t>((size_t)units * slot_stride * FT_TILE);
+  float2* vsz = ar.take<float2>((size_t)units * slot_stride * G);
+  KVLC_REQUIRE(s_part && wtiles && aimg && cimg && vsz, "flush workspace too small (%zu bytes)", ws_bytes);
+  float* p_part = s_part + (size_t)units * splits * D * RANK;
+  KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
+  prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
+  if ((rc = check_launch("prep_wtiles"))) return rc;
+  a.c = *c;
+  a.ad = *ad;
+  a.use_adapter = 1;
+  a.cpc = cpc;
+  a.s_out = s_part;
+  a.p_out = p_part;
+  a.splits = splits;
+  a.aimg = aimg;
+  a.cimg = cimg;
+  a.vsz = vsz;
+  a.slot_stride = slot_stride;
+  quant_kernel<<<dim3(max_nf, units), FT_THREADS, 0, s>>>(a, seq);
+  if ((rc = check_launch("quant"))) return rc;
+  KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
+  flush_tc_kernel<<<dim3(splits, units, 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
+  if ((rc = check_launch("flush_tc"))) return rc;
+  reduce_state_kernel<<<dim3(32, units), 256, 0, s>>>(*c, s_part, p_part, splits);
+  return check_launch("reduce_state");
+}
+
 int check_cache(const kvlc_cache* c) {
   KVLC_REQUIRE(c != nullptr, "null cache descriptor");
   KVLC_REQUIRE(c->B >= 1 && c->Hkv >= 1 && c->Hq >= c->Hkv && c->Hq % c->Hkv == 0 &&
@@ -1289,40 +1354,7 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
   }
   const bool use_ad = adapter_on(ad);
   if (max_nf > 0 && use_ad) {
-    // tensor-core path: one CTA per (unit, feature half, chunk range), <= one wave
-    static int sms = [] {
-      int dev = 0, n = 148;
-      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-      return n;
-    }();
-    const int ws_splits = (int)std::max<int64_t>(1, (n_tok / KVLC_G + 3) / 4);  // kvlc_prefill_workspace bound
-    // enough CTAs to fill whole waves (2 per unit-split: the feature halves), and at most 32
-    // chunks accumulated per TMEM partial: 63-chunk partials (an 8k sequence in a 128-unit
-    // batch) drifted to 1.3e-5 relative (T3 is 1e-5), 32-chunk ones measure 8e-6, 16-chunk
-    // ones 6e-6 but cost config 5 ~40 us in extra CTAs (tools/s_error_c2.py)
-#ifndef KVLC_TC_MAXCPC
-#define KVLC_TC_MAXCPC 32
-#endif
-    const int base = std::max({1, std::min(max_nf, sms / (2 * units)), (max_nf + KVLC_TC_MAXCPC - 1) / KVLC_TC_MAXCPC});
-    const int waves = (2 * units * base + sms - 1) / sms;  // one CTA per SM: fill the last wave
-    const int splits = std::min({ws_splits, std::max(1, max_nf), std::max(base, waves * sms / (2 * units))});
-    const int cpc = (max_nf + splits - 1) / splits;
-    Arena ar(ws, ws_bytes);
-    float* s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
-    uint8_t* wtiles = ar.take<uint8_t>((size_t)c->Hkv * 2 * 2 * FT_TILE);
-    const int slot_stride = (int)std::max<int64_t>(1, n_tok / KVLC_G);
-    uint8_t* aimg = ar.take<uint8_t>((size_t)units * slot_stride * 2 * FT_TILE);
-    uint8_t* cimg = ar.take<uint8_t>((size_t)units * slot_stride * FT_TILE);
-    float2* vsz = ar.take<float2>((size_t)units * slot_stride * G);
-    KVLC_REQUIRE(s_part && wtiles && aimg && cimg && vsz, "prefill workspace too small (%zu bytes)", ws_bytes);
-    float* p_part = s_part + (size_t)units * splits * D * RANK;
-    KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
-    prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
-    if ((rc = check_launch("prep_wtiles"))) return rc;
     FlushArgs a{};
-    a.c = *c;
-    a.ad = *ad;
-    a.use_adapter = 1;
     a.ksrc = k;
     a.vsrc = v;
     a.k_unit = n_tok * D;
@@ -1331,21 +1363,8 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
     a.v_unit = n_tok * D;
     a.v_t = D;
     a.v_c = 1;
-    a.cpc = cpc;
-    a.s_out = s_part;
-    a.p_out = p_part;
-    a.splits = splits;
-    a.aimg = aimg;
-    a.cimg = cimg;
-    a.vsz = vsz;
-    a.slot_stride = slot_stride;
-    quant_kernel<<<dim3(max_nf, units), FT_THREADS, 0, s>>>(a, seq);
-    if ((rc = check_launch("quant"))) return rc;
-    KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
-    flush_tc_kernel<<<dim3(splits, units, 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
-    if ((rc = check_launch("flush_tc"))) return rc;
-    reduce_state_kernel<<<dim3(32, units), 256, 0, s>>>(*c, s_part, p_part, splits);
-    if ((rc = check_launch("reduce_state"))) return rc;
+    a.ring = 0;
+    if ((rc = launch_tc_flush(c, ad, a, seq, max_nf, n_tok, ws, ws_bytes, s))) return rc;
   } else if (max_nf > 0) {
     // cpc chunks per CTA: enough CTAs to cover the SMs
     const int cpc = 4;
@@ -1373,11 +1392,11 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
   return check_launch("prefill");
 }
 
+size_t kvlc_append_workspace(const kvlc_cache* c) { return kvlc_prefill_workspace(c, KVLC_G); }
+
 int kvlc_append(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k_t, const uint16_t* v_t,
                 const int32_t* active_host, const int32_t* flush_host, void* ws, size_t ws_bytes,
                 void* stream) {
-  (void)ws;
-  (void)ws_bytes;
   KVLC_NEED_DEVICE();
   int rc = check_cache(c);
   if (rc) return rc;
@@ -1386,18 +1405,33 @@ int kvlc_append(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k_t
   static thread_local SeqInfo seq;
   memset(seq.active, 0, sizeof(seq.active));
   memset(seq.flush, 0, sizeof(seq.flush));
+  memset(seq.nflush, 0, sizeof(seq.nflush));
   bool any_flush = false;
   for (int b = 0; b < c->B; ++b) {
     if (!active_host || active_host[b]) seq.active[b >> 5] |= 1u << (b & 31);
     if (flush_host && flush_host[b]) {
       seq.flush[b >> 5] |= 1u << (b & 31);
+      seq.nflush[b] = 1;
       any_flush = true;
     }
   }
   const int units = c->B * c->Hkv;
   append_kernel<<<units, D, 0, s>>>(*c, k_t, v_t, seq);
   if ((rc = check_launch("append"))) return rc;
-  if (any_flush) {
+  if (any_flush && adapter_on(ad) && ws && ws_bytes >= kvlc_append_workspace(c)) {
+    // tensor-core flush of the due sequences' oldest G ring slots (quant_kernel in ring mode)
+    FlushArgs a{};
+    a.ksrc = c->kres;
+    a.vsrc = c->vres;
+    a.k_unit = (int64_t)SLOTS * D;
+    a.k_t = D;
+    a.k_c = 1;
+    a.v_unit = (int64_t)D * SLOTS;
+    a.v_t = 1;
+    a.v_c = SLOTS;
+    a.ring = 1;
+    if ((rc = launch_tc_flush(c, ad, a, seq, 1, KVLC_G, ws, ws_bytes, s))) return rc;
+  } else if (any_flush) {
     const bool use_ad = adapter_on(ad);
     FlushArgs a{};
     a.c = *c;
