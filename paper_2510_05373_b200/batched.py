@@ -135,8 +135,9 @@ class BatchedKVCache:
                          p(self.res_start_dev), p(self.res_len_dev))
 
     def _flush_ws(self, flush, adapters):
-        """(pointer, bytes) of the tensor-core flush workspace when an adapter flush is due."""
-        if not np.any(flush) or not _adapters_on(adapters):
+        """(pointer, bytes) of the tensor-core flush workspace when an adapter flush is due
+        (`_tc_flush = False` keeps the SIMT flush kernel: tests compare the two)."""
+        if not np.any(flush) or not _adapters_on(adapters) or not getattr(self, "_tc_flush", True):
             return None, 0
         ws = self.workspace(_lib.load().kvlc_append_workspace(ctypes.byref(self._struct)))
         return _ptr(ws), ws.numel()

@@ -277,3 +277,26 @@ def test_serving_step_graph_equals_eager_steps():
     assert np.array_equal(a.res_len, b.res_len)
     with pytest.raises(ValueError, match="eagerly"):
         step.replay()
+
+
+def test_ring_flush_tensor_core_and_simt_paths_agree():
+    """Decode-time flushes: the tensor-core path (kvlc_append with its workspace) and the SIMT
+    kernel (no workspace) produce identical code words / metadata and S, P within T3; both
+    match the oracle."""
+    B, Hkv, Hq, n = 2, 2, 8, 520
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=17)
+    oads = [orc.init_adapter(D, 256, seed=h) for h in range(Hkv)]
+    bank = AdapterBank.initialize(Hkv)
+    caches = []
+    for tc in (True, False):
+        cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+        cache._tc_flush = tc
+        for i in range(n):
+            cache.append(tdev(k[:, :, i]), tdev(v[:, :, i]), adapters=bank)
+        caches.append(cache)
+    ocs = oracle_caches(k, v, [n] * B, oads)
+    for cache in caches:
+        check_cache_exact(cache, ocs, [n] * B)
+        check_states(cache, ocs)
+    assert torch.equal(caches[0].kcodes, caches[1].kcodes) and torch.equal(caches[0].vcodes, caches[1].vcodes)
+    assert torch.equal(caches[0].vscale, caches[1].vscale) and torch.equal(caches[0].kzero, caches[1].kzero)
