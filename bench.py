@@ -279,7 +279,7 @@ def run_serving_loop(cache, q, bank, dev):
     cache.decode(q, adapters=bank, out=out)
     n = cache.steps_until_flush()
     for _ in range(3):
-        step.replay()
+        step.replay()                         # the first replay re-captures (the flush added a chunk)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()

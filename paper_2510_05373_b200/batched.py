@@ -294,28 +294,38 @@ class BatchedKVCache:
         """One steady-state decode-loop step in one CUDA graph: append k_t, v_t (one token
         per sequence, cache.py:120-130) then the fused decode of q.  Refill q / k_t / v_t
         in place and call `.replay()`; each replay advances the host length mirrors and
-        refuses to run into a flush (run that step eagerly: `append` then `decode`)."""
+        refuses to run into a flush (run that step eagerly: `append` then `decode`).  The
+        decode plan depends on the chunk counts, so after a flush the next replay
+        re-captures the graph."""
         if k_t.shape != (self.B, self.Hkv, D) or v_t.shape != k_t.shape:
             raise ValueError(f"token dims {tuple(k_t.shape)}/{tuple(v_t.shape)} != ({self.B}, {self.Hkv}, {D})")
         if out is None:
             out = torch.empty(q.shape, dtype=torch.bfloat16, device=self.device)
-        self.decode(q, adapters, out=out)  # sizes the decode workspace
-        torch.cuda.synchronize()
-        ad = _adapter_struct(adapters)
-        a_c = (ctypes.c_int32 * self.B)(*([1] * self.B))
-        f_c = (ctypes.c_int32 * self.B)(*([0] * self.B))
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            _lib.call("kvlc_append", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
-                      a_c, f_c, None, 0, _lib.stream_handle())
-            self.decode(q, adapters, out=out)
         cache = self
 
+        def capture():
+            cache.decode(q, adapters, out=out)  # sizes the decode workspace
+            torch.cuda.synchronize()
+            ad = _adapter_struct(adapters)
+            a_c = (ctypes.c_int32 * cache.B)(*([1] * cache.B))
+            f_c = (ctypes.c_int32 * cache.B)(*([0] * cache.B))
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                _lib.call("kvlc_append", ctypes.byref(cache._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
+                          a_c, f_c, None, 0, _lib.stream_handle())
+                cache.decode(q, adapters, out=out)
+            return graph, cache.n_chunks.copy()
+
         class _Step:
+            def __init__(self):
+                self.graph, self.chunks = capture()
+
             def replay(self):
                 if cache.steps_until_flush() < 1:
                     raise ValueError("a sequence flushes on this append: run the step eagerly")
-                graph.replay()
+                if not np.array_equal(self.chunks, cache.n_chunks):  # a flush changed the plan
+                    self.graph, self.chunks = capture()
+                self.graph.replay()
                 cache.res_len = cache.res_len + 1
 
         return _Step(), out

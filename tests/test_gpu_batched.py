@@ -264,19 +264,28 @@ def test_serving_step_graph_equals_eager_steps():
     kt = torch.empty((B, Hkv, D), dtype=torch.bfloat16, device="cuda")
     vt = torch.empty_like(kt)
     step, out = a.capture_serving_step(q, kt, vt, adapters=bank)
-    n_steps = a.steps_until_flush()
-    assert n_steps == 255 - (n0 - 128)
-    for i in range(n_steps):
+    assert a.steps_until_flush() == 255 - (n0 - 128)
+
+    def fill():
         q.copy_(tdev(g.standard_normal((B, Hq, D))))
         kt.copy_(tdev(g.standard_normal((B, Hkv, D))))
         vt.copy_(tdev(g.standard_normal((B, Hkv, D))))
-        step.replay()
+
+    for period in range(2):  # through a flush: the next replay re-captures with the new plan
+        for i in range(a.steps_until_flush()):
+            fill()
+            step.replay()
+            b.append(kt, vt, adapters=bank)
+            want = b.decode(q, adapters=bank)
+            assert torch.equal(out, want), (period, i)
+        assert np.array_equal(a.res_len, b.res_len)
+        with pytest.raises(ValueError, match="eagerly"):
+            step.replay()
+        fill()
+        a.append(kt, vt, adapters=bank)      # the flushing step, eagerly
         b.append(kt, vt, adapters=bank)
-        want = b.decode(q, adapters=bank)
-        assert torch.equal(out, want), i
-    assert np.array_equal(a.res_len, b.res_len)
-    with pytest.raises(ValueError, match="eagerly"):
-        step.replay()
+        assert torch.equal(a.decode(q, adapters=bank), b.decode(q, adapters=bank))
+    assert list(a.n_chunks) == [3, 3]
 
 
 def test_ring_flush_tensor_core_and_simt_paths_agree():
