@@ -686,9 +686,10 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     // KVLC_SPLIT_MINB CTAs per SM, at least 8 chunks per split, at most 52 records per
     // unit (the last CTA of a unit merges them all), then equal-length splits.
     // Configs 2 / 3 / 4: 7 -> 9 / 8 / 20 chunks, 49.2 -> 44.4 / 38.1 -> 34.8 / 55.6 -> 46.5 us.
+    // Rounded (not ceiled) wave target: 64 chunks per unit get 8 x 8 rather than 6 x 10 + 4.
     const long long slots = 148LL * KVLC_SPLIT_MINB;
     const long long chunks = (long long)p.U * std::max(span, 1);
-    long long t = std::max(8LL, (2 * chunks + 3 * slots - 1) / (3 * slots));
+    long long t = std::max(8LL, (4 * chunks + 3 * slots) / (6 * slots));  // round(chunks / (1.5 slots))
     t = std::max(t, (long long)(std::max(span, 1) + 51) / 52);
     const long long nsq = (std::max(span, 1) + t - 1) / t;
     cpc = (int)std::max(1LL, std::min(32LL, (std::max(span, 1) + nsq - 1) / nsq));
