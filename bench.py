@@ -297,7 +297,7 @@ def run_serving_loop(cache, q, bank, dev):
     return {"graph_step_us": step_us, "flush_step_us": flush_us,
             "us_per_step_amortised": (127 * step_us + flush_us) / 128,
             "note": "append + decode per step (steady state, second flush period); the flushing step "
-                    "(all 128 units, lockstep) runs eagerly with host launch overhead (SIMT flush kernel)"}
+                    "(all 128 units, lockstep) runs eagerly with host launch overhead (tensor-core ring flush)"}
 
 
 def run_other_configs(dev, peak_gbs):
