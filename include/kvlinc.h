@@ -227,8 +227,10 @@ typedef struct kvlc_decode_opts {
 
 /* Fused GQA decode (Algorithm 1 / decode_step_blocked, attention.py:197-276)
  * for every (b, q-head): q bf16 [B][Hq][128] -> out bf16 [B][Hq][128].
- * Launches phi_q and the split-KV kernel (PDL-chained); the last CTA of each
- * (b, kv-head) unit performs the LSE combine.  The workspace must be
+ * Launches the split-KV kernel (correction, quantized splits, residual
+ * window) and the LSE combine kernel, PDL-chained; plans with more than 64
+ * records per unit (explicit small chunks_per_split) fuse the combine into the
+ * last CTA of each (b, kv-head) unit instead.  The workspace must be
  * zero-filled before its first use (its head holds per-unit arrival counters
  * that every launch leaves at zero). */
 size_t kvlc_decode_workspace(const kvlc_cache* cache, const kvlc_decode_opts* o);

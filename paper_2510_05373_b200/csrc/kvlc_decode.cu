@@ -7,7 +7,7 @@
 // e^{-M}-consistent rule (_reduce_blocks, attention.py:158-194), the inverse
 // Hadamard rotation of the quantized numerator and the final divide.
 //
-// Kernels (one decode step = 1 launch):
+// Kernels (one decode step = 2 launches, PDL-chained):
 //   split_kernel    per CTA task, selected by blockIdx:
 //                   * correction (first, one per unit): phi_q of the unit's
 //                     query heads, C_d = P phi, C_n = S phi (attention.py:224-231)
@@ -18,9 +18,10 @@
 //                     (hi+lo fp16 split when the group has <= 4 heads)
 //                     (kvlc_quant.cuh)
 //                   * residual half: bf16 ring window, masked
-//                   the last CTA of each unit performs the LSE merge of the
-//                   unit's records + correction, the warp FWHT (H^T = H) and
-//                   the divide (no separate combine launch).
+//   combine_kernel  per (b, q-head): the LSE merge of the unit's records +
+//                   correction, the warp FWHT (H^T = H) and the divide.  Plans
+//                   with more than CMB_MAXREC records per unit fuse it instead
+//                   into the last arriving CTA of each unit (arrival counters).
 //
 // Online-softmax state is kept in log2 units (logit * log2 e); the sign of the
 // global max, which selects the correction branch, is unit independent.
@@ -108,6 +109,7 @@ struct DecArgs {
   int out_fp32;
   void* out;              // [B][Hq][D] bf16 / f32 (final output)
   float* rec_out;         // partial mode: [B][Hq][PREC] (split-KV across devices)
+  int sep_combine;        // 1: the combine is combine_kernel, PDL-chained (no arrival counters)
 };
 
 #include "kvlc_quant.cuh"
@@ -496,13 +498,14 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
     hd[j] = r < a.nrec ? __ldcg(reinterpret_cast<const float4*>(base + r * rstride))
                        : make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
   }
+  float mx = fmaxf(hd[0].x, hd[1].x), mtx = fmaxf(hd[0].z, hd[1].z);
   for (int r = 64 + lane; r < a.nrec; r += 32) {  // longer plans (explicit chunks_per_split)
     const float4 x = __ldcg(reinterpret_cast<const float4*>(base + r * rstride));
-    hd[1].x = fmaxf(hd[1].x, x.x);
-    hd[1].z = fmaxf(hd[1].z, x.z);
+    mx = fmaxf(mx, x.x);
+    mtx = fmaxf(mtx, x.z);
   }
-  float M = warp_max(fmaxf(hd[0].x, hd[1].x));
-  const float Mt = warp_max(fmaxf(hd[0].z, hd[1].z));
+  float M = warp_max(mx);
+  const float Mt = warp_max(mtx);
   float nr[4] = {0.f, 0.f, 0.f, 0.f}, nw[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
   if (M != -INFINITY) {
     for (int r0 = 0; r0 < a.nrec; r0 += 32) {
@@ -573,6 +576,27 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
 // task: quantized splits, residual halves, correction rows.  Every CTA bumps
 // its unit's arrival counter after publishing its record; the last one
 // performs the LSE combine of the unit (no separate combine launch).
+#ifdef KVLC_TRACE
+// per-CTA timeline (tools/trace_decode.py): globaltimer at entry, before the arrival
+// atomic and at exit, task kind (0 correction, 1 split, 2 residual), SM id
+constexpr int DT_MAX = 8192;
+__device__ unsigned long long g_dtrace[DT_MAX][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
+#define DT_STAMP(i, v) \
+  do { if (threadIdx.x == 0 && blockIdx.x < DT_MAX) g_dtrace[blockIdx.x][i] = (v); } while (0)
+#else
+#define DT_STAMP(i, v) do { } while (0)
+#endif
+
 template <int NG, int EXTRA>
 #ifndef KVLC_SPLIT_MINB
 #define KVLC_SPLIT_MINB 4
@@ -583,6 +607,9 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   const int U = a.c.B * a.c.Hkv;
   const int ncorr = a.tail && a.corr_on ? U : 0;  // correction CTAs first (their S stream overlaps)
   int x = blockIdx.x, unit;
+#ifdef KVLC_TRACE
+  const unsigned long long t_enter = gtimer();
+#endif
   if (x < ncorr) {
     unit = x;
     run_corr<NG>(a, unit, sm.rec);
@@ -594,6 +621,17 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
     unit = x / 2;
     run_resid<NG>(a, unit, x % 2, sm.rec);
   }
+#ifdef KVLC_TRACE
+  __syncthreads();
+  DT_STAMP(0, t_enter);
+  DT_STAMP(1, gtimer());
+  DT_STAMP(3, ((unsigned long long)smid() << 32) | (unsigned long long)((blockIdx.x < ncorr ? 0 : blockIdx.x < ncorr + U * a.nsq ? 1 : 2) << 24 | unit));
+  if (a.sep_combine) DT_STAMP(2, gtimer());
+#endif
+  if (a.sep_combine) {
+    griddep_launch();  // the combine kernel may be scheduled; it waits for this grid to complete
+    return;
+  }
   const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? 1 : 0) : 0);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -602,12 +640,116 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
     last = atomicAdd(a.done + unit, 1u) == (uint32_t)(per_unit - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) {
+    DT_STAMP(2, gtimer());
+    return;
+  }
   __threadfence();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = unit / a.c.Hkv, kvh = unit % a.c.Hkv;
   for (int h = warp; h < NG; h += WARPS) combine_head(a, NG, b, h, kvh, lane);
   if (threadIdx.x == 0) a.done[unit] = 0u;  // self-cleaning for the next step
+#ifdef KVLC_TRACE
+  __syncthreads();
+  DT_STAMP(2, gtimer() | (1ull << 63));  // top bit: this CTA ran the unit's combine
+#endif
+}
+
+// The LSE combine as its own launch (programmatic dependent of split_kernel), used when a
+// unit has at most CMB_MAXREC records: one CTA per (b, q-head), warp w takes records
+// w, w + 4, ..., lane l channels 4l .. 4l+3.  Every load (record numerators, headers,
+// correction row) is issued in one round after the split grid has completed; the
+// 4 warps' partial sums meet in shared memory and warp 0 applies the correction,
+// the FWHT and the divide (finish).
+constexpr int CMB_PER_WARP = 16;                  // numerators held in registers per lane
+constexpr int CMB_MAXREC = WARPS * CMB_PER_WARP;  // 64
+
+template <int NG>
+__global__ void __launch_bounds__(THREADS) combine_kernel(const DecArgs a) {
+  __shared__ float hm[CMB_MAXREC];   // record weights
+  __shared__ float red[3][WARPS];    // max m, max m_true, den
+  __shared__ __align__(16) float part[WARPS - 1][2][D];
+  const int gw = blockIdx.x, b = gw / a.c.Hq, qh = gw % a.c.Hq, kvh = qh / NG, hl = qh % NG;
+  const int unit = b * a.c.Hkv + kvh;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const float* base = a.rec + ((size_t)unit * a.nrec * NG + hl) * REC;
+  const size_t rs = (size_t)NG * REC;
+  const int nrec = a.nrec;
+  griddep_wait();
+  float4 y[CMB_PER_WARP];
+#pragma unroll
+  for (int i = 0; i < CMB_PER_WARP; ++i) {
+    const int r = warp + WARPS * i;
+    y[i] = r < nrec ? __ldcg(reinterpret_cast<const float4*>(base + r * rs + 4) + lane)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const float4 hd = t < nrec ? __ldcg(reinterpret_cast<const float4*>(base + t * rs))
+                             : make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
+  const float* corr = a.corr_on && !a.rec_out ? a.corr + (size_t)gw * (1 + D) : nullptr;
+  float cbuf[1 + 4];
+  if (corr && warp == 0) {
+    cbuf[0] = __ldcg(corr);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cbuf[1 + e] = __ldcg(corr + 1 + 4 * lane + e);
+  }
+  float m = warp_max(hd.x), mt = warp_max(hd.z);
+  if (lane == 0) {
+    red[0][warp] = m;
+    red[1][warp] = mt;
+  }
+  __syncthreads();
+  float M = red[0][0], Mt = red[1][0];
+#pragma unroll
+  for (int w = 1; w < WARPS; ++w) {
+    M = fmaxf(M, red[0][w]);
+    Mt = fmaxf(Mt, red[1][w]);
+  }
+  const float wt = hd.x == -INFINITY ? 0.f : exp2f(hd.x - M);
+  if (t < nrec) hm[t] = wt;
+  const float dsum = warp_sum(wt * hd.y);
+  if (lane == 0) red[2][warp] = dsum;
+  __syncthreads();
+  float nr[4] = {0.f, 0.f, 0.f, 0.f}, nw[4] = {0.f, 0.f, 0.f, 0.f};
+  if (M != -INFINITY) {
+#pragma unroll
+    for (int i = 0; i < CMB_PER_WARP; ++i) {
+      const int r = warp + WARPS * i;
+      if (r >= nrec) break;
+      const float w = hm[r];
+      float* acc = r < a.nsq ? nr : nw;  // quantized (rotated) vs residual (raw) basis
+      acc[0] = fmaf(w, y[i].x, acc[0]);
+      acc[1] = fmaf(w, y[i].y, acc[1]);
+      acc[2] = fmaf(w, y[i].z, acc[2]);
+      acc[3] = fmaf(w, y[i].w, acc[3]);
+    }
+  }
+  if (warp > 0) {
+    *reinterpret_cast<float4*>(&part[warp - 1][0][4 * lane]) = make_float4(nr[0], nr[1], nr[2], nr[3]);
+    *reinterpret_cast<float4*>(&part[warp - 1][1][4 * lane]) = make_float4(nw[0], nw[1], nw[2], nw[3]);
+  }
+  __syncthreads();
+  if (warp > 0) return;
+  float den = 0.f;
+#pragma unroll
+  for (int w = 0; w < WARPS; ++w) den += red[2][w];
+#pragma unroll
+  for (int w = 0; w < WARPS - 1; ++w) {
+    const float4 x = *reinterpret_cast<const float4*>(&part[w][0][4 * lane]);
+    const float4 z = *reinterpret_cast<const float4*>(&part[w][1][4 * lane]);
+    nr[0] += x.x; nr[1] += x.y; nr[2] += x.z; nr[3] += x.w;
+    nw[0] += z.x; nw[1] += z.y; nw[2] += z.z; nw[3] += z.w;
+  }
+  if (M == -INFINITY) den = 0.f;
+  if (a.rec_out) {  // partial mode: (M, den, Mt, 0, num_rot, num_raw), no correction
+    float* o = a.rec_out + (size_t)gw * PREC;
+    if (lane == 0) *reinterpret_cast<float4*>(o) = make_float4(M, den, Mt, 0.f);
+    *reinterpret_cast<float4*>(o + 4 + 4 * lane) = make_float4(nr[0], nr[1], nr[2], nr[3]);
+    *reinterpret_cast<float4*>(o + 4 + D + 4 * lane) = make_float4(nw[0], nw[1], nw[2], nw[3]);
+    return;
+  }
+  void* o = a.out_fp32 ? (void*)(static_cast<float*>(a.out) + (size_t)gw * D)
+                       : (void*)(static_cast<uint16_t*>(a.out) + (size_t)gw * D);
+  finish(M, Mt, den, nr, nw, corr ? cbuf : nullptr, a.literal, lane, o, a.out_fp32);
 }
 
 // Copies a step's input (q) from pinned host memory to the device with every 16-byte
@@ -690,7 +832,11 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     const long long slots = 148LL * KVLC_SPLIT_MINB;
     const long long chunks = (long long)p.U * std::max(span, 1);
     long long t = std::max(8LL, (4 * chunks + 3 * slots) / (6 * slots));  // round(chunks / (1.5 slots))
-    t = std::max(t, (long long)(std::max(span, 1) + 51) / 52);
+    static const int rec_cap = [] {
+      const char* e = getenv("KVLC_RECCAP");
+      return e ? atoi(e) : 52;
+    }();
+    t = std::max(t, (long long)(std::max(span, 1) + rec_cap - 1) / rec_cap);
     const long long nsq = (std::max(span, 1) + t - 1) / t;
     cpc = (int)std::max(1LL, std::min(32LL, (std::max(span, 1) + nsq - 1) / nsq));
   }
@@ -738,6 +884,15 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   a.out_fp32 = out_fp32;
   a.out = out;
   a.rec_out = rec_out;
+  // combine placement: its own PDL-chained kernel (config 2 / 3 / 4: 42.7 -> 40.1,
+  // 32.4 -> 27.4, 41.4 -> 35.1 us: the split CTAs skip the fence + arrival atomic, ~1.2 us
+  // each, and the combine is one load round per head, tools/trace_decode.py), or the last
+  // arriving CTA of each unit for plans with more records than combine_kernel holds
+  static const int sep_env = [] {  // KVLC_SEPCOMB=0 forces the fused combine (A/B)
+    const char* e = getenv("KVLC_SEPCOMB");
+    return e ? atoi(e) : 1;
+  }();
+  a.sep_combine = sep_env && p.nrec <= CMB_MAXREC;
   int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? p.U : 0) : 0);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -766,6 +921,10 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
       case 2: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 2>, a)); break;
       default: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 3>, a)); break;
     }
+  }
+  if (a.sep_combine) {
+    cfg.gridDim = dim3(c->B * c->Hq);
+    KVLC_CUDA(cudaLaunchKernelEx(&cfg, combine_kernel<NG>, a));
   }
   if (o && o->ev_end) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_end), s));
   return check_launch("decode");
@@ -800,6 +959,12 @@ bool adapter_active(const kvlc_adapter* ad) {
 }  // namespace kvlc
 
 using namespace kvlc;
+
+#ifdef KVLC_TRACE
+extern "C" int kvlc_dtrace_copy(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, g_dtrace, bytes < sizeof(g_dtrace) ? bytes : sizeof(g_dtrace)) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 extern "C" {
 

@@ -173,6 +173,23 @@ def test_split_partials_merge_equals_full_decode():
             assert e <= 2e-4, f"literal parts={parts} rel diff {e:.3e}"
 
 
+@pytest.mark.parametrize("cpc", [1, 2, 3])
+def test_explicit_split_plans_match_default(cpc):
+    # cpc 1: 81 records per unit (> 64: the combine is fused into the last CTA of each
+    # unit); cpc 2 / 3: 42 / 29 records (the PDL-chained combine kernel)
+    B, Hkv, Hq, n = 2, 2, 8, 80 * 128
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=21)
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k), tdev(v), lens=[n, n - 1000], adapters=bank)
+    qd = tdev(q)
+    for literal in (False, True):
+        ref = cache.decode(qd, adapters=bank, literal=literal, out_dtype=F32)
+        out = cache.decode(qd, adapters=bank, literal=literal, out_dtype=F32, chunks_per_split=cpc)
+        e = (out - ref).abs().max().item() / ref.abs().max().item()
+        assert e <= 2e-4, f"cpc={cpc} literal={literal} rel diff {e:.3e}"  # see the merge test above
+
+
 def test_correction_dominated_extremes():
     # all-ones keys, q = +-300: exp terms underflow and out ~ H^T C_n / C_d
     B, Hkv, Hq, n = 1, 1, 4, 700
