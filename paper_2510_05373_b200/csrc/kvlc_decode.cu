@@ -26,6 +26,7 @@
 // Online-softmax state is kept in log2 units (logit * log2 e); the sign of the
 // global max, which selects the correction branch, is unit independent.
 #include "kvlc_common.cuh"
+#include "kvlc_tc.cuh"
 
 #include <algorithm>
 #include <cstdlib>
@@ -612,7 +613,9 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
 #endif
   if (x < ncorr) {
     unit = x;
+#ifndef KVLC_PROBE_NOCORR  // probe build: correction CTAs exit at once (timing only)
     run_corr<NG>(a, unit, sm.rec);
+#endif
   } else if ((x -= ncorr) < U * a.nsq) {
     unit = x / a.nsq;
     run_quant<NG, EXTRA>(a, unit, x % a.nsq, sm);

@@ -2,9 +2,12 @@
 //
 // A quantized-split CTA owns chunks [lo, hi) of one (b, kv-head) unit.  Its
 // 4 warps take the 4 32-token slices of every chunk:
-//   * each warp streams its slice (1 KB of K codes, 1 KB of V codes, the
-//     slice's V scale/zero and the K scale/zero of its B-operand share)
-//     through a 3-stage cp.async pipeline in shared memory;
+//   * thread 0 streams whole chunks (4 KB K codes, 4 KB V codes, 4 x 256 B
+//     scales / zeros, the bytes of the global layouts) into a STAGES-deep ring
+//     of shared-memory stages with bulk copies (TMA, one transaction-count
+//     mbarrier per stage; 4 warp arrivals free a stage): up to STAGES - 1 chunks
+//     in flight per CTA without LSU request tracking (per-warp 16-B cp.async
+//     streaming topped out near 3.3 TB/s with the math removed);
 //   * the QK^T B operand of a chunk (q' = q * s_k, fp16 hi/lo) and the zero
 //     term zt = q . z_k are built cooperatively (warp w: k-tiles 2w, 2w+1) into
 //     shared buffers guarded by full / empty mbarriers (4 warp arrivals each):
@@ -19,7 +22,7 @@
 #pragma once
 
 #ifndef KVLC_STAGES
-#define KVLC_STAGES 3
+#define KVLC_STAGES 4
 #endif
 constexpr int STAGES = KVLC_STAGES;
 constexpr float LAZY = 8.f;
@@ -57,37 +60,22 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src));
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// One warp's data for one chunk.
-struct WarpStage {
-  uint4 k[2][32];   // K words 0-3 / 4-7 of each lane (fragment-native layout)
-  uint4 v[2][32];   // V words
-  uint2 vs[8];      // V scales of tokens 32w + 4g .. +3, per g
-  uint2 vz[8];
-  uint2 ks[8];      // K scales of channels 32w .. 32w+31 (the warp's B share)
-  uint2 kz[8];
+// One chunk of one unit in shared memory: the bytes of the global layouts.
+struct ChunkStage {
+  uint4 k[WARPS][32][2];   // fragment-native K words of warp slice w, lane l: words 0-3 / 4-7
+  uint4 v[WARPS][32][2];   // V words
+  uint16_t vs[128], vz[128], ks[128], kz[128];   // fp16 V scale / zero per token, K per channel
 };
 
 struct QuantSmem {
-  WarpStage stage[STAGES][WARPS];
+  ChunkStage stage[STAGES];
   uint4 bq[NBUF][4][32];   // [buf][k-tile pair][lane]: (b0, b1 of kt = 2p, b0, b1 of kt = 2p+1)
   uint4 bl[NBUF][4][32];   // low parts (groups of > 4 heads)
   float4 zt[NBUF][8];      // [buf][column g] -> partial zero terms of the 4 warps
   uint64_t full[NBUF];     // 4 warp arrivals: every share of the buffer's B is written
   uint64_t empty[NBUF];    // 4 warp arrivals: every warp is done reading the buffer
+  uint64_t sfull[STAGES];  // bulk-copy transaction count: the stage's chunk has landed
+  uint64_t sempty[STAGES]; // 4 warp arrivals: the stage's chunk is consumed
 };
 
 // CTA-scope mbarriers between the 4 warps of a quantized split (one elected lane per
@@ -121,43 +109,28 @@ union SplitSmem {
   float rec[WARPS * 8 * REC];
 };
 
-// Per-lane source pointers of a warp's slice; every lane issues the same
-// cp.async sequence (2 x 16 B K, 2 x 16 B V, one 8 B metadata piece: lanes
-// 0-7 V scales, 8-15 V zeros, 16-23 K scales, 24-31 K zeros).  All sources
-// advance by a fixed stride per chunk.
-struct SliceSrc {
-  const uint4* k;     // advances 256 uint4 (4 KB) per chunk
-  const uint4* v;
-  const uint2* meta;  // advances 32 uint2 (256 B) per chunk
-  __device__ __forceinline__ void init(const kvlc_cache& c, size_t cb, int warp, int lane) {
-    k = reinterpret_cast<const uint4*>(c.kcodes + ((cb * 4 + warp) * 32 + lane) * 8);
-    v = reinterpret_cast<const uint4*>(c.vcodes + ((cb * 4 + warp) * 32 + lane) * 8);
-    const int role = lane >> 3, sub = lane & 7;
-    const uint16_t* base = role == 0 ? c.vscale : role == 1 ? c.vzero : role == 2 ? c.kscale : c.kzero;
-    meta = reinterpret_cast<const uint2*>(base + cb * 128 + 32 * warp + 4 * sub);
-  }
-  __device__ __forceinline__ void issue(WarpStage& st, int lane, int chunk_off) const {
-    const uint4* kp = k + (size_t)chunk_off * 256;
-    const uint4* vp = v + (size_t)chunk_off * 256;
-    cp_async16(&st.k[0][lane], kp);
-    cp_async16(&st.k[1][lane], kp + 1);
-    cp_async16(&st.v[0][lane], vp);
-    cp_async16(&st.v[1][lane], vp + 1);
-    cp_async8(&st.vs[0] + lane, meta + (size_t)chunk_off * 32);   // vs, vz, ks, kz are contiguous
-  }
-};
+// Thread 0: chunk cb (absolute) into stage `st`, completion on `bar`.
+__device__ __forceinline__ void issue_chunk(const kvlc_cache& c, size_t cb, ChunkStage& st, uint64_t* bar) {
+  tc::mbar_expect_tx(bar, (uint32_t)sizeof(ChunkStage));
+  tc::bulk_g2s(st.k, c.kcodes + cb * 1024, 4096, bar);
+  tc::bulk_g2s(st.v, c.vcodes + cb * 1024, 4096, bar);
+  tc::bulk_g2s(st.vs, c.vscale + cb * 128, 256, bar);
+  tc::bulk_g2s(st.vz, c.vzero + cb * 128, 256, bar);
+  tc::bulk_g2s(st.ks, c.kscale + cb * 128, 256, bar);
+  tc::bulk_g2s(st.kz, c.kzero + cb * 128, 256, bar);
+}
 
 // Builds this warp's share (k-tiles 2w, 2w+1) of a chunk's B operand from its stage.
 //  HILO: column n = g holds head g>>1: the hi part for even g, the lo part
 //        (exact FMA residual q*s - hi) for odd g.
 //  else: column n = g holds head g (hi in bq, lo in bl).
 template <int NG>
-__device__ __forceinline__ void build_b(QuantSmem& sm, int buf, const WarpStage& st,
+__device__ __forceinline__ void build_b(QuantSmem& sm, int buf, const ChunkStage& st,
                                         const uint32_t (&qs)[4], int warp, int lane) {
   constexpr bool HILO = NG <= 4;
   const int g = lane >> 2, t = lane & 3;
-  const uint32_t* ks = reinterpret_cast<const uint32_t*>(st.ks);
-  const uint32_t* kz = reinterpret_cast<const uint32_t*>(st.kz);
+  const uint32_t* ks = reinterpret_cast<const uint32_t*>(st.ks + 32 * warp);
+  const uint32_t* kz = reinterpret_cast<const uint32_t*>(st.kz + 32 * warp);
   uint32_t b[4], bl[4];
   float zp = 0.f;
 #pragma unroll
@@ -189,8 +162,8 @@ __device__ __forceinline__ void build_b(QuantSmem& sm, int buf, const WarpStage&
 // tokens 32w+4g+j at bits 2j; V word 4mt+p holds tokens 32w+8t+2mt+{0,1,4,5}
 // in bytes 0..3 and channels 32p+8j+g at bits 2j.
 template <int NG, int EXTRA>
-__device__ __forceinline__ void quant_chunk(const WarpStage& stg, const QuantSmem& sm, int buf,
-                                            WarpState<NG>& st, int lane) {
+__device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSmem& sm, int buf,
+                                            WarpState<NG>& st, int warp, int lane) {
   constexpr bool HILO = NG <= 4;
   constexpr int NH = WarpState<NG>::NH;
   constexpr bool QK_LO = !HILO && (EXTRA & 1);
@@ -211,7 +184,7 @@ __device__ __forceinline__ void quant_chunk(const WarpStage& stg, const QuantSme
 #pragma unroll
     for (int j = 0; j < 4; ++j) cq[i][j] = 0.f;
   {
-    const uint4 k0 = stg.k[0][lane], k1 = stg.k[1][lane];
+    const uint4 k0 = stg.k[warp][lane][0], k1 = stg.k[warp][lane][1];
     const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
@@ -291,7 +264,8 @@ __device__ __forceinline__ void quant_chunk(const WarpStage& stg, const QuantSme
       }
     }
   }
-  const uint2 vs = stg.vs[g], vz = stg.vz[g];
+  const uint2 vs = reinterpret_cast<const uint2*>(stg.vs + 32 * warp)[g];
+  const uint2 vz = reinterpret_cast<const uint2*>(stg.vz + 32 * warp)[g];
   const float2 s01 = __half22float2(u2h(vs.x)), s23 = __half22float2(u2h(vs.y));
   const float2 z01 = __half22float2(u2h(vz.x)), z23 = __half22float2(u2h(vz.y));
   const float svs[4] = {s01.x, s01.y, s23.x, s23.y}, svz[4] = {z01.x, z01.y, z23.x, z23.y};
@@ -328,7 +302,7 @@ __device__ __forceinline__ void quant_chunk(const WarpStage& stg, const QuantSme
   }
 
   // ---- P V: 8 channel tiles x the slice's 2 token tiles ----
-  const uint4 v0 = stg.v[0][lane], v1 = stg.v[1][lane];
+  const uint4 v0 = stg.v[warp][lane][0], v1 = stg.v[warp][lane][1];
   const uint32_t vw[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
@@ -452,20 +426,22 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
   const size_t cb0 = (size_t)unit * c.max_chunks;
   QuantSmem& q = sm.quant;
   if (threadIdx.x < 2 * NBUF) qb_init(threadIdx.x < NBUF ? &q.full[threadIdx.x] : &q.empty[threadIdx.x - NBUF], WARPS);
-  __syncthreads();  // barriers initialised before any warp arrives
-  SliceSrc src;
-  src.init(c, cb0 + lo, warp, lane);
-  // prologue: stages for chunks 0, 1 (relative) issued before the sequence length and
-  // q arrive, so the three round trips overlap; bounded by the cache capacity (always
-  // allocated), only chunks below the sequence's count are consumed
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (lo + s < cap_hi) src.issue(q.stage[s][warp], lane, s);
-    cp_commit();
+  // prologue: chunks 0 .. STAGES-2 (relative) requested before the sequence length and q
+  // arrive, so the round trips overlap; bounded by the cache capacity (always allocated),
+  // only chunks below the sequence's count are consumed, the rest drained at the end
+  const int n_pro = max(0, min(STAGES - 1, cap_hi - lo));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&q.sfull[s], 1);
+      tc::mbar_init(&q.sempty[s], WARPS);
+    }
+    tc::mbar_fence_init();
+    for (int s = 0; s < n_pro; ++s) issue_chunk(c, cb0 + lo + s, q.stage[s], &q.sfull[s]);
   }
+  __syncthreads();  // barriers initialised before any warp waits or arrives
   const int hi = min(n_ch, lo + a.cpc);
-  if (lo < hi) {
-    const int n = hi - lo;
+  const int n = max(0, hi - lo);
+  if (n > 0) {
     // q (fp16, exact from bf16) for this warp's B share: column n = g,
     // channels 32w + 16e + 2t + {0,1} (+8)
     uint32_t qs[4];
@@ -482,32 +458,40 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
       for (int i = 0; i < 4; ++i)
         qs[i] = h2u(__floats2half2_rn(__uint_as_float(raw[i] << 16), __uint_as_float(raw[i] & 0xffff0000u)));
     }
-    cp_wait<STAGES - 2>();
-    __syncwarp();
-    build_b<NG>(q, 0, q.stage[0][warp], qs, warp, lane);
+    tc::mbar_wait(&q.sfull[0], 0u);
+#ifndef KVLC_PROBE_NOMATH  // probe build: the stream and barriers without the math (timing only)
+    build_b<NG>(q, 0, q.stage[0], qs, warp, lane);
+#endif
     qb_arrive(&q.full[0], lane);
-    int s_cur = 0;
     for (int k = 0; k < n; ++k) {
-      const int buf = k % NBUF;
-      const int s_next = s_cur == STAGES - 1 ? 0 : s_cur + 1;
-      const int s_fill = s_cur == 0 ? STAGES - 1 : s_cur - 1;   // freed by chunk k-1 (this warp's own)
-      if (k + STAGES - 1 < n) src.issue(q.stage[s_fill][warp], lane, k + STAGES - 1);
-      cp_commit();
+      const int buf = k % NBUF, s_cur = k % STAGES;
       qb_wait(&q.full[buf], (uint32_t)(k / NBUF) & 1u);   // every share of chunk k's B
-      quant_chunk<NG, EXTRA>(q.stage[s_cur][warp], q, buf, st, lane);
+      // every warp has consumed chunk k-1 (its B share of chunk k follows that): refill its stage
+      if (threadIdx.x == 0 && k + STAGES - 1 < n) {
+        const int j = k + STAGES - 1, s = j % STAGES;
+        if (k >= 1) tc::mbar_wait(&q.sempty[s], (uint32_t)((k - 1) / STAGES) & 1u);
+        issue_chunk(c, cb0 + lo + j, q.stage[s], &q.sfull[s]);
+      }
+#ifndef KVLC_PROBE_NOMATH
+      quant_chunk<NG, EXTRA>(q.stage[s_cur], q, buf, st, warp, lane);
+#endif
+      qb_arrive(&q.sempty[s_cur], lane);
       qb_arrive(&q.empty[buf], lane);
       if (k + 1 < n) {
-        cp_wait<STAGES - 2>();   // chunk k+1 has landed (only k+2 may be pending)
-        __syncwarp();
-        const int nb = (k + 1) % NBUF;
+        const int nb = (k + 1) % NBUF, s_next = (k + 1) % STAGES;
+        tc::mbar_wait(&q.sfull[s_next], (uint32_t)((k + 1) / STAGES) & 1u);
         if (k + 1 >= NBUF) qb_wait(&q.empty[nb], (uint32_t)((k + 1) / NBUF - 1) & 1u);  // chunk k+1-NBUF done
-        build_b<NG>(q, nb, q.stage[s_next][warp], qs, warp, lane);
+#ifndef KVLC_PROBE_NOMATH
+        build_b<NG>(q, nb, q.stage[s_next], qs, warp, lane);
+#endif
         qb_arrive(&q.full[nb], lane);
       }
-      s_cur = s_next;
     }
   }
-  cp_wait<0>();      // also drains a speculative prologue of an empty split
+  // drain speculative prologue chunks that were not consumed (their bytes land in the
+  // record area below)
+  if (threadIdx.x == 0)
+    for (int j = n; j < n_pro; ++j) tc::mbar_wait(&q.sfull[j % STAGES], (uint32_t)(j / STAGES) & 1u);
   __syncthreads();   // the record area aliases the pipeline buffers
   warp_store<NG, true>(st, sm.rec + warp * NG * REC, lane);
   __syncthreads();
