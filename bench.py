@@ -38,7 +38,7 @@ REPLICAS = 4   # rotating caches: 4 x 101 MB > 126 MB L2, every step streams fro
 
 
 def algo_bytes_step(b, hkv, hq, nq, nr):
-    """One decode step = one split_kernel launch: packed K/V codes, fp16
+    """One decode step = split_kernel + combine_kernel: packed K/V codes, fp16
     scale / zero, bf16 residual window, fp32 S and P, q / out bf16 per unit, W1q / W2q
     per kv head."""
     g = hq // hkv
@@ -127,7 +127,7 @@ def run_ours(args, rank, world, local_rank):
     for i in range(W):
         caches[i % REPLICAS].decode(q, adapters=bank, out=out)
     torch.cuda.synchronize()
-    # one CUDA graph per replica: the step's single split_kernel launch
+    # one CUDA graph per replica: the step's split_kernel + combine_kernel (PDL pair)
     graphs = [c.capture_decode(q, adapters=bank, out=out)[0] for c in caches]
     for i in range(W):
         graphs[i % REPLICAS].replay()
@@ -218,7 +218,8 @@ def run_ours(args, rank, world, local_rank):
         "hbm_gbs_step": step_bytes / (step_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
                      "frac": achieved / peak_gbs, "traffic": traffic,
-                     "kernel": "split_kernel (kvlc_decode.cu)", "split_us": split_ms * 1e3,
+                     "kernel": "split_kernel + combine_kernel (kvlc_decode.cu, the PDL-chained pair "
+                               "of one step; traffic: split_kernel)", "split_us": split_ms * 1e3,
                      "algorithmic_bytes_per_launch": step_bytes,
                      "timing": f"mean of {KG}-launch CUDA graph replays (back to back, L2-cold replicas)",
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
@@ -226,12 +227,14 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": B * world / (e2e_ms * 1e-3), "unit": "tokens/s",
                 "h2d_bytes_per_step": B * HQ * D * 2, "d2h_bytes_per_step": B * HQ * D * 2,
                 "ms_per_step": e2e_ms,
-                "path": "BatchedKVCache.capture_decode(q_host=, out_host=): pinned-host q H2D copy, "
-                        "split_kernel whose combine stores out into pinned host memory, one CUDA graph "
-                        "launch per step"},
-        "gpu_launches": K,
-        "launch": "CUDA graph per step: one split_kernel launch (correction CTAs incl. phi_q, "
-                  "quantized splits, residual halves; LSE combine fused into the last CTA of each unit)",
+                "path": "BatchedKVCache.capture_decode(q_host=, out_host=): kvlc_stage_input copies "
+                        "q from pinned host memory, split_kernel, combine_kernel stores out into pinned "
+                        "host memory; one CUDA graph launch per step (3 kernels, PDL-chained)",
+                "gpu_launches": 3 * K},
+        "gpu_launches": 2 * K,
+        "launch": "CUDA graph per step: split_kernel (correction CTAs incl. phi_q, quantized splits "
+                  "streaming whole chunks by TMA bulk copies, residual halves) + combine_kernel "
+                  "(LSE merge per (b, q-head)), chained by programmatic dependent launch",
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_fa:
