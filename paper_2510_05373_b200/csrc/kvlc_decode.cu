@@ -96,7 +96,10 @@ struct DecArgs {
   const uint16_t* q;      // [B][Hq][D] bf16
   const float* w1q;       // [Hkv][D][HALF] fp32 (phi_q weights, adapter.py:91-93)
   const float* w2q;
-  float* corr;            // [B][Hq][1 + D]  (C_d, C_n)
+  float* corr;            // [2][B][Hq][1 + D]: (C_d, C_n) partials of the two feature halves
+  size_t corr_half;       // B * Hq * (1 + D)
+  float* corr_ext;        // partial mode: the caller's [B][Hq][1 + D] (the halves' sum)
+  int corr_split;         // correction CTAs per unit: 1 (run_corr_unit) or 2 (run_corr halves)
   float* rec;             // [U][nrec][NG][REC]
   int nsq;                // quantized split CTAs per unit
   int cpc;                // chunks per quantized-split CTA
@@ -237,13 +240,14 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
   cta_merge<NG>(smrec, a.rec + ((size_t)unit * a.nrec + a.nsq + hf) * NG * REC);
 }
 
-// Correction of one unit (attention.py:224-231): phi_q of the unit's NG query heads
+// Correction of one unit by one CTA (both feature halves; used when the splits and these
+// CTAs fit one wave, see corr_split): phi_q of the unit's NG query heads
 // (feature_map, adapter.py:80-88: thread t owns feature t of each half, W columns
 // read from L2 8 channels per round trip), then C_d = P . phi and C_n = S phi for all
 // 128 rows of S (8 / 4 rows per warp per pass, lanes across the 256 features).  These
 // CTAs come first in the grid, so their S stream overlaps the code stream.
 template <int NG>
-__device__ void run_corr(const DecArgs& a, int unit, float* smf) {
+__device__ void run_corr_unit(const DecArgs& a, int unit, float* smf) {
   static_assert(HALF == THREADS, "one feature of each half per thread");
   const kvlc_cache& c = a.c;
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
@@ -261,12 +265,7 @@ __device__ void run_corr(const DecArgs& a, int unit, float* smf) {
   for (int i = 0; i < NG; ++i) z[0][i] = z[1][i] = 0.f;
   const float* W1 = a.w1q + (size_t)kvh * D * HALF + t;
   const float* W2 = a.w2q + (size_t)kvh * D * HALF + t;
-#ifndef KVLC_PHI_BATCH
-#define KVLC_PHI_BATCH 8
-#endif
-  // channels per batch of W loads in flight: 16 / 32 measured slower for the whole kernel
-  // (43.1 vs 44.7 us, the larger unrolled body costs the shared quantized-split code)
-  constexpr int PB = KVLC_PHI_BATCH;
+  constexpr int PB = 8;  // channels per batch of W1 + W2 loads in flight (16 / 32 measured slower)
 #pragma unroll 1
   for (int c0 = 0; c0 < D; c0 += PB) {
     float w1[PB], w2[PB];
@@ -405,6 +404,153 @@ __device__ void run_corr(const DecArgs& a, int unit, float* smf) {
   }
 }
 
+// Correction of one unit, feature half h (attention.py:224-231): phi_q of the unit's NG
+// query heads over half h (feature_map, adapter.py:80-88: the softmax is per half, so the
+// halves are independent; thread t owns feature t, W_h columns read from L2 KVLC_PHI_BATCH
+// channels per round trip), then the half's partial C_d = P_h . phi_h and C_n = S[:, h] phi_h
+// (RPW rows per warp per pass, lanes across the 128 features, one reduce-scatter per 32
+// values).  Two CTAs per unit halve the longest task of the grid (a whole-unit CTA ran
+// ~18 us against ~14 us splits and set the tail, tools/trace_decode.py); the combine adds
+// the halves.  These CTAs come first in the grid, so their S stream overlaps the codes.
+template <int NG>
+__device__ void run_corr(const DecArgs& a, int unit, int h, float* smf) {
+  static_assert(HALF == THREADS, "one feature of the half per thread");
+  const kvlc_cache& c = a.c;
+  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const size_t qh0 = (size_t)b * c.Hq + (size_t)kvh * NG;
+  float* corr = a.corr + (size_t)h * a.corr_half;
+  float* qs = smf;                 // [NG][D]
+  float* phs = qs + NG * D;        // [NG][HALF]
+  float* red = phs + NG * HALF;    // [WARPS][NG]
+  float* stat = red + WARPS * NG;  // [NG]
+  griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
+  for (int i = t; i < NG * D; i += THREADS) qs[i] = bf2f(a.q[(qh0 + i / D) * D + i % D]);
+  __syncthreads();
+  float z[NG];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) z[i] = 0.f;
+  const float* W = (h ? a.w2q : a.w1q) + (size_t)kvh * D * HALF + t;
+#ifndef KVLC_PHI_BATCH
+#define KVLC_PHI_BATCH 16
+#endif
+  constexpr int PB = KVLC_PHI_BATCH;  // channels of W loads in flight per thread
+#pragma unroll 1
+  for (int c0 = 0; c0 < D; c0 += PB) {
+    float w[PB];
+#pragma unroll
+    for (int k = 0; k < PB; ++k) w[k] = __ldg(W + (size_t)(c0 + k) * HALF);
+#pragma unroll
+    for (int k = 0; k < PB; k += 4) {
+#pragma unroll
+      for (int i = 0; i < NG; ++i) {
+        const float4 x = *reinterpret_cast<const float4*>(qs + i * D + c0 + k);
+        z[i] = fmaf(x.x, w[k], z[i]);
+        z[i] = fmaf(x.y, w[k + 1], z[i]);
+        z[i] = fmaf(x.z, w[k + 2], z[i]);
+        z[i] = fmaf(x.w, w[k + 3], z[i]);
+      }
+    }
+  }
+  // max-shifted softmax of the half (linalg.py:38-47)
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const float m = warp_max(z[i]);
+    if (lane == 0) red[warp * NG + i] = m;
+  }
+  __syncthreads();
+  if (t < NG) {
+    float m = red[t];
+#pragma unroll
+    for (int w = 1; w < WARPS; ++w) m = fmaxf(m, red[w * NG + t]);
+    stat[t] = m;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NG; ++i) z[i] = expf(z[i] - stat[i]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const float sm_ = warp_sum(z[i]);
+    if (lane == 0) red[warp * NG + i] = sm_;
+  }
+  __syncthreads();
+  if (t < NG) {
+    float sm_ = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) sm_ += red[w * NG + t];
+    stat[t] = sm_;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NG; ++i) phs[i * HALF + t] = z[i] / stat[i];
+  __syncthreads();
+
+  float ph[NG][4];  // features 4 lane .. 4 lane + 3 of the half
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const float4 x = *reinterpret_cast<const float4*>(phs + i * HALF + lane * 4);
+    ph[i][0] = x.x; ph[i][1] = x.y; ph[i][2] = x.z; ph[i][3] = x.w;
+  }
+  if (warp == 0) {  // C_d partial = P_h . phi_h (attention.py:228)
+    const float4 x = __ldg(reinterpret_cast<const float4*>(c.P + (size_t)unit * RANK + h * HALF + lane * 4));
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      float v = x.x * ph[i][0];
+      v = fmaf(x.y, ph[i][1], v);
+      v = fmaf(x.z, ph[i][2], v);
+      v = fmaf(x.w, ph[i][3], v);
+      v = warp_sum(v);
+      if (lane == 0) corr[(qh0 + i) * (1 + D)] = v;
+    }
+  }
+  // C_n partial = S[:, h] phi_h (attention.py:227): per pass a warp takes RPW rows; per-lane
+  // partial dots, then one reduce-scatter per 32 values (lane L ends with value L's total)
+  constexpr int RPW = NG > 4 ? 4 : 8;  // rows per warp per pass (register budget at 8 heads)
+  constexpr int NV = RPW * NG;
+  constexpr int NB = (NV + 31) / 32;
+#pragma unroll 1
+  for (int row0 = warp * RPW; row0 < D; row0 += WARPS * RPW) {
+    float4 sr[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+      sr[r] = __ldg(reinterpret_cast<const float4*>(c.S + ((size_t)unit * D + row0 + r) * RANK + h * HALF + lane * 4));
+    float vals[NB * 32];
+#pragma unroll
+    for (int n = 0; n < NB * 32; ++n) vals[n] = 0.f;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+      for (int i = 0; i < NG; ++i) {
+        float v = sr[r].x * ph[i][0];
+        v = fmaf(sr[r].y, ph[i][1], v);
+        v = fmaf(sr[r].z, ph[i][2], v);
+        v = fmaf(sr[r].w, ph[i][3], v);
+        vals[r * NG + i] = v;
+      }
+    }
+#pragma unroll
+    for (int blk = 0; blk < NB; ++blk) {
+      float* x = vals + 32 * blk;
+#pragma unroll
+      for (int sft = 16; sft >= 1; sft >>= 1) {
+        const bool upper = lane & sft;
+#pragma unroll
+        for (int k = 0; k < sft; ++k) {
+          const float send = upper ? x[k] : x[k + sft];
+          const float keep = upper ? x[k + sft] : x[k];
+          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
+      }
+      const int n = 32 * blk + lane;
+      if (n < NV) {
+        const int r = n / NG, i = n % NG;
+        corr[(qh0 + i) * (1 + D) + 1 + row0 + r] = x[0];
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------ combine ----
 // FWHT of 128 values, 4 per lane (channels 4 lane + e), unnormalised.
 __device__ __forceinline__ void warp_fwht128(float (&x)[4], int lane) {
@@ -478,6 +624,25 @@ __device__ __forceinline__ void finish(float M, float Mt, float den, float (&nr)
     *reinterpret_cast<uint2*>(static_cast<uint16_t*>(out) + 4 * lane) =
         make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
   }
+}
+
+// Correction of (b, q-head) gw, the two feature halves' partials summed (written by
+// other CTAs of the split grid: read through L2); lane: {C_d, C_n[4 lane .. 4 lane + 3]}
+__device__ __forceinline__ void load_corr(const DecArgs& a, size_t gw, int lane, float (&cb)[5]) {
+  const float* c0 = a.corr + gw * (1 + D);
+  const float* c1 = c0 + a.corr_half;
+  const bool two = a.corr_split == 2;
+  cb[0] = two ? __ldcg(c0) + __ldcg(c1) : __ldcg(c0);
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    cb[1 + e] = two ? __ldcg(c0 + 1 + 4 * lane + e) + __ldcg(c1 + 1 + 4 * lane + e) : __ldcg(c0 + 1 + 4 * lane + e);
+}
+// partial mode: the summed correction row into the caller's buffer
+__device__ __forceinline__ void store_corr_ext(const DecArgs& a, size_t gw, int lane, const float (&cb)[5]) {
+  float* o = a.corr_ext + gw * (1 + D);
+  if (lane == 0) o[0] = cb[0];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o[1 + 4 * lane + e] = cb[1 + e];
 }
 
 // LSE merge of one (b, q-head)'s split records (+ the correction) by one warp:
@@ -554,23 +719,19 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
     }
     den = warp_sum(den);
   }
-  if (a.rec_out) {  // partial mode: (M, den, Mt, 0, num_rot, num_raw), no correction
+  float cbuf[1 + 4];
+  if (a.corr_on) load_corr(a, gw, lane, cbuf);
+  if (a.rec_out) {  // partial mode: (M, den, Mt, 0, num_rot, num_raw), correction to corr_ext
     float* o = a.rec_out + (size_t)gw * PREC;
     if (lane == 0) *reinterpret_cast<float4*>(o) = make_float4(M, den, Mt, 0.f);
     *reinterpret_cast<float4*>(o + 4 + 4 * lane) = make_float4(nr[0], nr[1], nr[2], nr[3]);
     *reinterpret_cast<float4*>(o + 4 + D + 4 * lane) = make_float4(nw[0], nw[1], nw[2], nw[3]);
+    if (a.corr_on && a.corr_ext) store_corr_ext(a, gw, lane, cbuf);
     return;
   }
   void* o = a.out_fp32 ? (void*)(static_cast<float*>(a.out) + (size_t)gw * D)
                        : (void*)(static_cast<uint16_t*>(a.out) + (size_t)gw * D);
-  const float* corr = a.corr_on ? a.corr + (size_t)gw * (1 + D) : nullptr;
-  float cbuf[1 + 4];
-  if (corr) {  // correction rows were written by other CTAs: read through L2
-    cbuf[0] = __ldcg(corr);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) cbuf[1 + e] = __ldcg(corr + 1 + 4 * lane + e);  // rows are 129 floats
-  }
-  finish(M, Mt, den, nr, nw, corr ? cbuf : nullptr, a.literal, lane, o, a.out_fp32);
+  finish(M, Mt, den, nr, nw, a.corr_on ? cbuf : nullptr, a.literal, lane, o, a.out_fp32);
 }
 
 // The whole decode step's split-KV work in one launch; blockIdx selects the
@@ -606,15 +767,18 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   __shared__ __align__(16) SplitSmem sm;
   __shared__ int last;
   const int U = a.c.B * a.c.Hkv;
-  const int ncorr = a.tail && a.corr_on ? U : 0;  // correction CTAs first (their S stream overlaps)
+  const int ncorr = a.tail && a.corr_on ? a.corr_split * U : 0;  // correction CTAs first (S overlaps codes)
   int x = blockIdx.x, unit;
 #ifdef KVLC_TRACE
   const unsigned long long t_enter = gtimer();
 #endif
   if (x < ncorr) {
-    unit = x;
+    unit = a.corr_split == 2 ? x >> 1 : x;
 #ifndef KVLC_PROBE_NOCORR  // probe build: correction CTAs exit at once (timing only)
-    run_corr<NG>(a, unit, sm.rec);
+    if (a.corr_split == 2)
+      run_corr<NG>(a, unit, x & 1, sm.rec);
+    else
+      run_corr_unit<NG>(a, unit, sm.rec);
 #endif
   } else if ((x -= ncorr) < U * a.nsq) {
     unit = x / a.nsq;
@@ -635,7 +799,7 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
     griddep_launch();  // the combine kernel may be scheduled; it waits for this grid to complete
     return;
   }
-  const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? 1 : 0) : 0);
+  const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? a.corr_split : 0) : 0);
   __syncthreads();
   if (threadIdx.x == 0) {
     griddep_wait();   // the predecessor grid (if any) has flushed: counters / q are current
@@ -688,13 +852,8 @@ __global__ void __launch_bounds__(THREADS) combine_kernel(const DecArgs a) {
   }
   const float4 hd = t < nrec ? __ldcg(reinterpret_cast<const float4*>(base + t * rs))
                              : make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
-  const float* corr = a.corr_on && !a.rec_out ? a.corr + (size_t)gw * (1 + D) : nullptr;
   float cbuf[1 + 4];
-  if (corr && warp == 0) {
-    cbuf[0] = __ldcg(corr);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) cbuf[1 + e] = __ldcg(corr + 1 + 4 * lane + e);
-  }
+  if (a.corr_on && warp == 0) load_corr(a, gw, lane, cbuf);
   float m = warp_max(hd.x), mt = warp_max(hd.z);
   if (lane == 0) {
     red[0][warp] = m;
@@ -743,16 +902,17 @@ __global__ void __launch_bounds__(THREADS) combine_kernel(const DecArgs a) {
     nw[0] += z.x; nw[1] += z.y; nw[2] += z.z; nw[3] += z.w;
   }
   if (M == -INFINITY) den = 0.f;
-  if (a.rec_out) {  // partial mode: (M, den, Mt, 0, num_rot, num_raw), no correction
+  if (a.rec_out) {  // partial mode: (M, den, Mt, 0, num_rot, num_raw), correction to corr_ext
     float* o = a.rec_out + (size_t)gw * PREC;
     if (lane == 0) *reinterpret_cast<float4*>(o) = make_float4(M, den, Mt, 0.f);
     *reinterpret_cast<float4*>(o + 4 + 4 * lane) = make_float4(nr[0], nr[1], nr[2], nr[3]);
     *reinterpret_cast<float4*>(o + 4 + D + 4 * lane) = make_float4(nw[0], nw[1], nw[2], nw[3]);
+    if (a.corr_on && a.corr_ext) store_corr_ext(a, gw, lane, cbuf);
     return;
   }
   void* o = a.out_fp32 ? (void*)(static_cast<float*>(a.out) + (size_t)gw * D)
                        : (void*)(static_cast<uint16_t*>(a.out) + (size_t)gw * D);
-  finish(M, Mt, den, nr, nw, corr ? cbuf : nullptr, a.literal, lane, o, a.out_fp32);
+  finish(M, Mt, den, nr, nw, a.corr_on ? cbuf : nullptr, a.literal, lane, o, a.out_fp32);
 }
 
 // Copies a step's input (q) from pinned host memory to the device with every 16-byte
@@ -849,7 +1009,7 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   p.nrec = p.nsq + (tail ? 2 : 0);
   size_t BH = (size_t)c->B * c->Hq;
   p.corr_off = 0;
-  p.rec_off = align_up(BH * (1 + D) * sizeof(float));
+  p.rec_off = align_up(2 * BH * (1 + D) * sizeof(float));  // correction partials of the 2 halves
   // arrival counters first: their offset must not depend on the split plan
   // (they are zero-initialised once and left at zero by every launch)
   p.done_off = 0;
@@ -864,7 +1024,7 @@ template <int NG>
 int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, const Plan& p,
               char* ws, int chunk_lo, int chunk_hi, int tail, float* corr_ext, int literal,
               int out_fp32, void* out, float* rec_out, const kvlc_decode_opts* o, cudaStream_t s) {
-  float* corr = corr_ext ? corr_ext : reinterpret_cast<float*>(ws + p.corr_off);
+  float* corr = reinterpret_cast<float*>(ws + p.corr_off);  // the halves; the combine sums them
   float* rec = reinterpret_cast<float*>(ws + p.rec_off);
   DecArgs a{};
   a.c = *c;
@@ -874,6 +1034,8 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     a.w2q = ad->w2q;
   }
   a.corr = corr;
+  a.corr_half = (size_t)c->B * c->Hq * (1 + D);
+  a.corr_ext = corr_ext;
   a.rec = rec;
   a.nsq = p.nsq;
   a.cpc = p.cpc;
@@ -896,7 +1058,16 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     return e ? atoi(e) : 1;
   }();
   a.sep_combine = sep_env && p.nrec <= CMB_MAXREC;
-  int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? p.U : 0) : 0);
+  // correction halves (two CTAs per unit) shorten the grid's longest task; they pay only
+  // when the splits spill past one wave anyway (config 2: 38.0 -> 37.3 us; config 3, whose
+  // splits + whole-unit corrections fit one wave: 26.6 -> 30.9 us with halves)
+  static const int corr_split_env = [] {  // KVLC_CORRSPLIT=1/2 forces (A/B)
+    const char* e = getenv("KVLC_CORRSPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  a.corr_split = corr_split_env ? corr_split_env
+                                : ((long long)p.U * (p.nsq + 1) > 148LL * KVLC_SPLIT_MINB ? 2 : 1);
+  int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? a.corr_split * p.U : 0) : 0);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
