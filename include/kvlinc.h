@@ -230,7 +230,11 @@ typedef struct kvlc_decode_opts {
  * Launches the split-KV kernel (correction, quantized splits, residual
  * window) and the LSE combine kernel, PDL-chained; plans with more than 64
  * records per unit (explicit small chunks_per_split) fuse the combine into the
- * last CTA of each (b, kv-head) unit instead.  The workspace must be
+ * last CTA of each (b, kv-head) unit instead.  The launch may overlap the
+ * previous kernel on `stream` (programmatic dependent launch): q may be
+ * produced by any kernel; cache state must be written through this library
+ * (prefill / append / flush_due / deserialize_unit mark the stream so that the
+ * next decode on it waits fully).  The workspace must be
  * zero-filled before its first use (its head holds per-unit arrival counters
  * that every launch leaves at zero). */
 size_t kvlc_decode_workspace(const kvlc_cache* cache, const kvlc_decode_opts* o);

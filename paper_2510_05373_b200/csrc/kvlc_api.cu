@@ -43,6 +43,35 @@ bool device_ok() {
   return cached == 1;
 }
 
+// The decode launch overlaps the previous kernel on its stream (programmatic dependent
+// launch) and issues cache reads (code stream, chunk counts, residual window) before
+// griddepcontrol.wait.  Entry points that write cache state mark their stream; the next
+// decode on a marked stream launches without the overlap.  Per host thread, last 8 streams.
+namespace {
+thread_local void* tl_dirty[8];
+thread_local int tl_ndirty = 0;
+}  // namespace
+
+void note_cache_write(void* stream) {
+  for (int i = 0; i < tl_ndirty; ++i)
+    if (tl_dirty[i] == stream) return;
+  if (tl_ndirty < 8) {
+    tl_dirty[tl_ndirty++] = stream;
+  } else {
+    for (int i = 1; i < 8; ++i) tl_dirty[i - 1] = tl_dirty[i];
+    tl_dirty[7] = stream;
+  }
+}
+
+bool take_cache_write(void* stream) {
+  for (int i = 0; i < tl_ndirty; ++i)
+    if (tl_dirty[i] == stream) {
+      tl_dirty[i] = tl_dirty[--tl_ndirty];
+      return true;
+    }
+  return false;
+}
+
 }  // namespace kvlc
 
 extern "C" {

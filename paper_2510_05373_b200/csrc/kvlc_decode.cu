@@ -131,6 +131,7 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  griddep_wait();  // the ring and its window may come from a programmatic-launch predecessor (append)
   const int start = c.res_start[b], len = c.res_len[b];
   const int base = 128 * hf + 32 * warp;
   WarpState<NG> st;
@@ -143,7 +144,6 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
     const uint16_t* vr = c.vres + (size_t)unit * D * SLOTS;
     // q (bf16) B fragments: column n = g; channels 32kp + 8t + 4e + {0,1 | 2,3}
     uint32_t qb[4][4];
-    griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
     {
       const int head = HILO ? (g >> 1) : g;
       const bool valid = HILO ? ((g & 1) == 0 && head < NG) : head < NG;
@@ -1072,14 +1072,16 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
   cfg.stream = s;
-  // programmatic dependent launch: CTAs may start while a predecessor kernel (e.g. the
-  // kvlc_stage_input copy of q) finishes; every read of q or of the arrival counters
-  // follows griddepcontrol.wait, the code streams do not
+  // programmatic dependent launch: CTAs may start while the predecessor kernel (the
+  // previous step's combine, or kvlc_stage_input's copy of q) finishes; every read of q or
+  // of the arrival counters follows griddepcontrol.wait, the code streams do not, so after
+  // an entry point that wrote cache state (prefill / append / flush / deserialize) the
+  // launch waits fully (take_cache_write)
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = take_cache_write(s) ? 0 : 1;  // the predecessor wrote cache state: full wait
   if (o && o->ev_begin) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_begin), s));
   if (NG <= 4) {
     KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a));

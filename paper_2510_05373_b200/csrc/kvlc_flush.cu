@@ -1415,6 +1415,10 @@ int kvlc_append(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k_t
       any_flush = true;
     }
   }
+  // a flush writes codes / chunk counts, which the next decode reads before its
+  // griddepcontrol.wait: that decode must not overlap (a plain append only moves the
+  // residual ring, read after the wait)
+  if (any_flush) kvlc::note_cache_write(stream);
   const int units = c->B * c->Hkv;
   append_kernel<<<units, D, 0, s>>>(*c, k_t, v_t, seq);
   if ((rc = check_launch("append"))) return rc;
@@ -1479,6 +1483,7 @@ int kvlc_serialize_unit(const kvlc_cache* c, int32_t unit, int32_t n_chunks, int
 
 int kvlc_deserialize_unit(const kvlc_cache* c, int32_t unit, const uint8_t* image, int32_t n_chunks,
                           int32_t res_len, int32_t rank, void* stream) {
+  kvlc::note_cache_write(stream);  // no PDL overlap for the next decode on this stream
   KVLC_NEED_DEVICE();
   int rc = check_cache(c);
   if (rc) return rc;
