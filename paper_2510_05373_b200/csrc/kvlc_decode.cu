@@ -432,9 +432,9 @@ __device__ void run_corr(const DecArgs& a, int unit, int h, float* smf) {
   for (int i = 0; i < NG; ++i) z[i] = 0.f;
   const float* W = (h ? a.w2q : a.w1q) + (size_t)kvh * D * HALF + t;
 #ifndef KVLC_PHI_BATCH
-#define KVLC_PHI_BATCH 16
+#define KVLC_PHI_BATCH 32
 #endif
-  constexpr int PB = KVLC_PHI_BATCH;  // channels of W loads in flight per thread
+  constexpr int PB = KVLC_PHI_BATCH;  // channels of W loads in flight per thread (16: +0.1 us, same registers)
 #pragma unroll 1
   for (int c0 = 0; c0 < D; c0 += PB) {
     float w[PB];
