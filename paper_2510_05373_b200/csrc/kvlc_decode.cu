@@ -425,7 +425,13 @@ __device__ void run_corr(const DecArgs& a, int unit, int h, float* smf) {
   float* red = phs + NG * HALF;    // [WARPS][NG]
   float* stat = red + WARPS * NG;  // [NG]
   griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
-  for (int i = t; i < NG * D; i += THREADS) qs[i] = bf2f(a.q[(qh0 + i / D) * D + i % D]);
+  {  // all NG loads in flight before the shared-memory stores
+    uint16_t qv[NG];
+#pragma unroll
+    for (int i = 0; i < NG; ++i) qv[i] = __ldg(a.q + (qh0 + i) * D + t);
+#pragma unroll
+    for (int i = 0; i < NG; ++i) qs[i * D + t] = bf2f(qv[i]);
+  }
   __syncthreads();
   float z[NG];
 #pragma unroll
