@@ -22,14 +22,15 @@
 #pragma once
 
 #ifndef KVLC_STAGES
-#define KVLC_STAGES 4
+#define KVLC_STAGES 3   // with 3 B buffers: kernel pair 34.9 -> 34.6 us vs 4 stages / 2 buffers
 #endif
 constexpr int STAGES = KVLC_STAGES;
 constexpr float LAZY = 8.f;
 #ifndef KVLC_BBUF
-#define KVLC_BBUF 2
+#define KVLC_BBUF 3
 #endif
-constexpr int NBUF = KVLC_BBUF;   // B-operand buffers (3 / 4 measured equal: tools/run_dec.sh)
+constexpr int NBUF = KVLC_BBUF;   // B-operand buffers: a warp refills a buffer once every warp is
+                                  // done with the chunk NBUF back (static shared memory <= 48 KB)
 
 template <int NG>
 struct WarpState {
