@@ -142,6 +142,34 @@ def test_append_stream_crosses_flushes():
     assert np.abs(out - ref).max() <= 1e-3 * np.abs(ref).max()
 
 
+def test_decode_right_after_flushing_append():
+    # decode is launched with programmatic dependent launch and streams codes before its
+    # griddepcontrol.wait; after an append that flushes, the library launches it without
+    # the overlap.  No host sync between the steps: every output is read
+    # at the end and checked against the oracle state of its step.
+    B, Hkv, Hq = 2, 2, 8
+    lens0 = [254, 126]
+    steps = 4
+    n = max(lens0) + steps
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=31)
+    oads = [orc.init_adapter(D, 256, seed=h) for h in range(Hkv)]
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k[:, :, :max(lens0)]), tdev(v[:, :, :max(lens0)]), lens=lens0, adapters=bank)
+    pos, outs, lens_at = list(lens0), [], []
+    qd = tdev(q)
+    for s in range(steps):
+        kt = np.stack([k[b, :, pos[b]] for b in range(B)])
+        vt = np.stack([v[b, :, pos[b]] for b in range(B)])
+        cache.append(tdev(kt), tdev(vt), adapters=bank)   # step 1 flushes sequence 0 (R + G)
+        pos = [p + 1 for p in pos]
+        outs.append(cache.decode(qd, adapters=bank, out_dtype=F32))
+        lens_at.append(list(pos))
+    for out, lens in zip(outs, lens_at):
+        ref = oracle_decode(q, oracle_caches(k, v, lens, oads), oads)
+        assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3 * np.abs(ref).max(), lens
+
+
 def test_split_partials_merge_equals_full_decode():
     B, Hkv, Hq, n = 2, 2, 8, 1500
     k, v, q = make_inputs(B, Hkv, Hq, n, seed=3)
