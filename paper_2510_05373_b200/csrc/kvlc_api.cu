@@ -2,6 +2,7 @@
 #include "kvlc_common.cuh"
 
 #include <mutex>
+#include <unordered_set>
 
 namespace kvlc {
 
@@ -44,32 +45,25 @@ bool device_ok() {
 }
 
 // The decode launch overlaps the previous kernel on its stream (programmatic dependent
-// launch) and issues cache reads (code stream, chunk counts, residual window) before
-// griddepcontrol.wait.  Entry points that write cache state mark their stream; the next
-// decode on a marked stream launches without the overlap.  Per host thread, last 8 streams.
+// launch) and issues its first chunks' code copies before griddepcontrol.wait.  Entry
+// points that write codes or chunk counts mark the CACHE (keyed by its code buffer, so
+// the mark is independent of host thread and stream); the next decode of a marked cache
+// launches without the overlap and clears the mark.  Writers outside the library call
+// kvlc_note_cache_write().
 namespace {
-thread_local void* tl_dirty[8];
-thread_local int tl_ndirty = 0;
+std::mutex g_dirty_mu;
+std::unordered_set<const void*> g_dirty;
 }  // namespace
 
-void note_cache_write(void* stream) {
-  for (int i = 0; i < tl_ndirty; ++i)
-    if (tl_dirty[i] == stream) return;
-  if (tl_ndirty < 8) {
-    tl_dirty[tl_ndirty++] = stream;
-  } else {
-    for (int i = 1; i < 8; ++i) tl_dirty[i - 1] = tl_dirty[i];
-    tl_dirty[7] = stream;
-  }
+void note_cache_write(const kvlc_cache* c) {
+  if (!c) return;
+  std::lock_guard<std::mutex> lock(g_dirty_mu);
+  g_dirty.insert(c->kcodes);
 }
 
-bool take_cache_write(void* stream) {
-  for (int i = 0; i < tl_ndirty; ++i)
-    if (tl_dirty[i] == stream) {
-      tl_dirty[i] = tl_dirty[--tl_ndirty];
-      return true;
-    }
-  return false;
+bool take_cache_write(const kvlc_cache* c) {
+  std::lock_guard<std::mutex> lock(g_dirty_mu);
+  return g_dirty.erase(c->kcodes) > 0;
 }
 
 }  // namespace kvlc
@@ -81,5 +75,7 @@ int kvlc_version(void) { return 10000; /* 1.0.0 */ }
 const char* kvlc_last_error(void) { return kvlc::g_err; }
 
 int kvlc_device_ok(void) { return kvlc::device_ok() ? 1 : 0; }
+
+void kvlc_note_cache_write(const kvlc_cache* c) { kvlc::note_cache_write(c); }
 
 }  // extern "C"

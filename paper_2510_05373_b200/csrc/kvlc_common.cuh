@@ -40,8 +40,8 @@ bool device_ok();
   } while (0)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
-void note_cache_write(void* stream);   // kvlc_api.cu: the next decode on `stream` waits fully
-bool take_cache_write(void* stream);   // true (and cleared) if `stream` was marked
+void note_cache_write(const kvlc_cache* c);  // kvlc_api.cu: the next decode of `c` waits fully
+bool take_cache_write(const kvlc_cache* c);  // true (and cleared) if `c` was marked
 
 inline int lane_bits(int bits) { return bits == 2 ? 2 : (bits == 8 ? 8 : 4); }
 inline int lanes_per_word(int bits) { return 32 / lane_bits(bits); }

@@ -117,6 +117,7 @@ struct DecArgs {
 };
 
 #include "kvlc_quant.cuh"
+#include "kvlc_quant_wpc.cuh"
 
 // Residual window half hf: ring slots [128 hf, 128 hf + 128), 32 per warp.
 __device__ __forceinline__ int res_sigma(int r) {  // QK row -> slot offset within a 16-slot tile
@@ -404,6 +405,77 @@ __device__ void run_corr_unit(const DecArgs& a, int unit, float* smf) {
   }
 }
 
+// The half's C_d = P_h . phi_h and C_n = S[:, h] phi_h partials (attention.py:227-228) from
+// phi_h in shared memory (phs [NG][HALF]).
+template <int NG>
+__device__ __forceinline__ void corr_half_dots(const DecArgs& a, int unit, int h, const float* phs, float* corr,
+                                               size_t qh0, int warp, int lane) {
+  const kvlc_cache& c = a.c;
+  float ph[NG][4];  // features 4 lane .. 4 lane + 3 of the half
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const float4 x = *reinterpret_cast<const float4*>(phs + i * HALF + lane * 4);
+    ph[i][0] = x.x; ph[i][1] = x.y; ph[i][2] = x.z; ph[i][3] = x.w;
+  }
+  if (warp == 0) {  // C_d partial = P_h . phi_h (attention.py:228)
+    const float4 x = __ldg(reinterpret_cast<const float4*>(c.P + (size_t)unit * RANK + h * HALF + lane * 4));
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      float v = x.x * ph[i][0];
+      v = fmaf(x.y, ph[i][1], v);
+      v = fmaf(x.z, ph[i][2], v);
+      v = fmaf(x.w, ph[i][3], v);
+      v = warp_sum(v);
+      if (lane == 0) corr[(qh0 + i) * (1 + D)] = v;
+    }
+  }
+  // C_n partial = S[:, h] phi_h (attention.py:227): per pass a warp takes RPW rows; per-lane
+  // partial dots, then one reduce-scatter per 32 values (lane L ends with value L's total)
+  constexpr int RPW = NG > 4 ? 4 : 8;  // rows per warp per pass (register budget at 8 heads)
+  constexpr int NV = RPW * NG;
+  constexpr int NB = (NV + 31) / 32;
+#pragma unroll 1
+  for (int row0 = warp * RPW; row0 < D; row0 += WARPS * RPW) {
+    float4 sr[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+      sr[r] = __ldg(reinterpret_cast<const float4*>(c.S + ((size_t)unit * D + row0 + r) * RANK + h * HALF + lane * 4));
+    float vals[NB * 32];
+#pragma unroll
+    for (int n = 0; n < NB * 32; ++n) vals[n] = 0.f;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+#pragma unroll
+      for (int i = 0; i < NG; ++i) {
+        float v = sr[r].x * ph[i][0];
+        v = fmaf(sr[r].y, ph[i][1], v);
+        v = fmaf(sr[r].z, ph[i][2], v);
+        v = fmaf(sr[r].w, ph[i][3], v);
+        vals[r * NG + i] = v;
+      }
+    }
+#pragma unroll
+    for (int blk = 0; blk < NB; ++blk) {
+      float* x = vals + 32 * blk;
+#pragma unroll
+      for (int sft = 16; sft >= 1; sft >>= 1) {
+        const bool upper = lane & sft;
+#pragma unroll
+        for (int k = 0; k < sft; ++k) {
+          const float send = upper ? x[k] : x[k + sft];
+          const float keep = upper ? x[k + sft] : x[k];
+          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
+      }
+      const int n = 32 * blk + lane;
+      if (n < NV) {
+        const int r = n / NG, i = n % NG;
+        corr[(qh0 + i) * (1 + D) + 1 + row0 + r] = x[0];
+      }
+    }
+  }
+}
+
 // Correction of one unit, feature half h (attention.py:224-231): phi_q of the unit's NG
 // query heads over half h (feature_map, adapter.py:80-88: the softmax is per half, so the
 // halves are independent; thread t owns feature t, W_h columns read from L2 KVLC_PHI_BATCH
@@ -492,69 +564,100 @@ __device__ void run_corr(const DecArgs& a, int unit, int h, float* smf) {
   for (int i = 0; i < NG; ++i) phs[i * HALF + t] = z[i] / stat[i];
   __syncthreads();
 
-  float ph[NG][4];  // features 4 lane .. 4 lane + 3 of the half
+  corr_half_dots<NG>(a, unit, h, phs, corr, qh0, warp, lane);
+}
+
+// Correction half h with the weights staged by TMA (warp-per-chunk kernel: its CTAs hold
+// 72 KB of dynamic shared memory): W_h (64 KB, L2-resident, shared by the batch) lands in
+// shared memory in one round trip instead of 128 / KVLC_PHI_BATCH dependent L2 load
+// rounds, and the half's S columns are prefetched into L2 at CTA start so the C_n pass
+// reads them from L2 (the whole-CTA time was ~10 us of load latency, r02 trace).
+template <int NG>
+__device__ void run_corr_staged(const DecArgs& a, int unit, int h, unsigned char* smem) {
+  static_assert(HALF == THREADS, "one feature of the half per thread");
+  const kvlc_cache& c = a.c;
+  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const size_t qh0 = (size_t)b * c.Hq + (size_t)kvh * NG;
+  float* corr = a.corr + (size_t)h * a.corr_half;
+  float* Ws = reinterpret_cast<float*>(smem);  // [D][HALF] W_h, then phs [NG][HALF]
+  float* qs = Ws + D * HALF;                    // [NG][D]
+  float* red = qs + NG * D;                     // [WARPS][NG]
+  float* stat = red + WARPS * NG;               // [NG]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stat + 8);
+  const float* Wg = (h ? a.w2q : a.w1q) + (size_t)kvh * D * HALF;
+  if (t == 0) {
+    tc::mbar_init(bar, 1);
+    tc::mbar_fence_init();
+    tc::mbar_expect_tx(bar, (uint32_t)(D * HALF * sizeof(float)));
 #pragma unroll
-  for (int i = 0; i < NG; ++i) {
-    const float4 x = *reinterpret_cast<const float4*>(phs + i * HALF + lane * 4);
-    ph[i][0] = x.x; ph[i][1] = x.y; ph[i][2] = x.z; ph[i][3] = x.w;
+    for (int p = 0; p < 4; ++p)
+      tc::bulk_g2s(Ws + p * (D * HALF / 4), Wg + p * (D * HALF / 4), (uint32_t)(D * HALF), bar);
   }
-  if (warp == 0) {  // C_d partial = P_h . phi_h (attention.py:228)
-    const float4 x = __ldg(reinterpret_cast<const float4*>(c.P + (size_t)unit * RANK + h * HALF + lane * 4));
+  // row t of the half's S columns (512 B) into L2 while phi_q is computed
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;\n" ::"l"(c.S + ((size_t)unit * D + t) * RANK + h * HALF)
+               : "memory");
+  griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
+  {
+    uint16_t qv[NG];
+#pragma unroll
+    for (int i = 0; i < NG; ++i) qv[i] = __ldg(a.q + (qh0 + i) * D + t);
+#pragma unroll
+    for (int i = 0; i < NG; ++i) qs[i * D + t] = bf2f(qv[i]);
+  }
+  __syncthreads();  // q in shared memory, barrier initialised
+  tc::mbar_wait(bar, 0u);
+  float z[NG];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) z[i] = 0.f;
+#pragma unroll 4
+  for (int c0 = 0; c0 < D; c0 += 4) {
+    const float w0 = Ws[(c0 + 0) * HALF + t], w1 = Ws[(c0 + 1) * HALF + t];
+    const float w2 = Ws[(c0 + 2) * HALF + t], w3 = Ws[(c0 + 3) * HALF + t];
 #pragma unroll
     for (int i = 0; i < NG; ++i) {
-      float v = x.x * ph[i][0];
-      v = fmaf(x.y, ph[i][1], v);
-      v = fmaf(x.z, ph[i][2], v);
-      v = fmaf(x.w, ph[i][3], v);
-      v = warp_sum(v);
-      if (lane == 0) corr[(qh0 + i) * (1 + D)] = v;
+      const float4 x = *reinterpret_cast<const float4*>(qs + i * D + c0);
+      z[i] = fmaf(x.x, w0, z[i]);
+      z[i] = fmaf(x.y, w1, z[i]);
+      z[i] = fmaf(x.z, w2, z[i]);
+      z[i] = fmaf(x.w, w3, z[i]);
     }
   }
-  // C_n partial = S[:, h] phi_h (attention.py:227): per pass a warp takes RPW rows; per-lane
-  // partial dots, then one reduce-scatter per 32 values (lane L ends with value L's total)
-  constexpr int RPW = NG > 4 ? 4 : 8;  // rows per warp per pass (register budget at 8 heads)
-  constexpr int NV = RPW * NG;
-  constexpr int NB = (NV + 31) / 32;
-#pragma unroll 1
-  for (int row0 = warp * RPW; row0 < D; row0 += WARPS * RPW) {
-    float4 sr[RPW];
+  // max-shifted softmax of the half (linalg.py:38-47)
 #pragma unroll
-    for (int r = 0; r < RPW; ++r)
-      sr[r] = __ldg(reinterpret_cast<const float4*>(c.S + ((size_t)unit * D + row0 + r) * RANK + h * HALF + lane * 4));
-    float vals[NB * 32];
-#pragma unroll
-    for (int n = 0; n < NB * 32; ++n) vals[n] = 0.f;
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-#pragma unroll
-      for (int i = 0; i < NG; ++i) {
-        float v = sr[r].x * ph[i][0];
-        v = fmaf(sr[r].y, ph[i][1], v);
-        v = fmaf(sr[r].z, ph[i][2], v);
-        v = fmaf(sr[r].w, ph[i][3], v);
-        vals[r * NG + i] = v;
-      }
-    }
-#pragma unroll
-    for (int blk = 0; blk < NB; ++blk) {
-      float* x = vals + 32 * blk;
-#pragma unroll
-      for (int sft = 16; sft >= 1; sft >>= 1) {
-        const bool upper = lane & sft;
-#pragma unroll
-        for (int k = 0; k < sft; ++k) {
-          const float send = upper ? x[k] : x[k + sft];
-          const float keep = upper ? x[k + sft] : x[k];
-          x[k] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
-        }
-      }
-      const int n = 32 * blk + lane;
-      if (n < NV) {
-        const int r = n / NG, i = n % NG;
-        corr[(qh0 + i) * (1 + D) + 1 + row0 + r] = x[0];
-      }
-    }
+  for (int i = 0; i < NG; ++i) {
+    const float m = warp_max(z[i]);
+    if (lane == 0) red[warp * NG + i] = m;
   }
+  __syncthreads();  // also: every thread is done with W_h (phs reuses its space)
+  if (t < NG) {
+    float m = red[t];
+#pragma unroll
+    for (int w = 1; w < WARPS; ++w) m = fmaxf(m, red[w * NG + t]);
+    stat[t] = m;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NG; ++i) z[i] = expf(z[i] - stat[i]);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    const float sm_ = warp_sum(z[i]);
+    if (lane == 0) red[warp * NG + i] = sm_;
+  }
+  __syncthreads();
+  if (t < NG) {
+    float sm_ = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) sm_ += red[w * NG + t];
+    stat[t] = sm_;
+  }
+  __syncthreads();
+  float* phs = Ws;
+#pragma unroll
+  for (int i = 0; i < NG; ++i) phs[i * HALF + t] = z[i] / stat[i];
+  __syncthreads();
+  corr_half_dots<NG>(a, unit, h, phs, corr, qh0, warp, lane);
 }
 
 // ------------------------------------------------------------ combine ----
@@ -765,12 +868,15 @@ __device__ __forceinline__ uint32_t smid() {
 #define DT_STAMP(i, v) do { } while (0)
 #endif
 
-template <int NG, int EXTRA>
 #ifndef KVLC_SPLIT_MINB
 #define KVLC_SPLIT_MINB 4
 #endif
-__global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const DecArgs a) {
-  __shared__ __align__(16) SplitSmem sm;
+// WPC: quantized splits run warp per chunk (kvlc_quant_wpc.cuh, dynamic shared memory)
+// instead of warp per 32-token slice (kvlc_quant.cuh, static shared memory)
+template <int NG, int EXTRA, bool WPC>
+__device__ __forceinline__ void split_body(const DecArgs& a, unsigned char* smem) {
+  SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem);
+  float* const smrec = reinterpret_cast<float*>(smem);
   __shared__ int last;
   const int U = a.c.B * a.c.Hkv;
   const int ncorr = a.tail && a.corr_on ? a.corr_split * U : 0;  // correction CTAs first (S overlaps codes)
@@ -781,18 +887,23 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   if (x < ncorr) {
     unit = a.corr_split == 2 ? x >> 1 : x;
 #ifndef KVLC_PROBE_NOCORR  // probe build: correction CTAs exit at once (timing only)
-    if (a.corr_split == 2)
-      run_corr<NG>(a, unit, x & 1, sm.rec);
+    if (a.corr_split == 2 && WPC)
+      run_corr_staged<NG>(a, unit, x & 1, smem);
+    else if (a.corr_split == 2)
+      run_corr<NG>(a, unit, x & 1, smrec);
     else
-      run_corr_unit<NG>(a, unit, sm.rec);
+      run_corr_unit<NG>(a, unit, smrec);
 #endif
   } else if ((x -= ncorr) < U * a.nsq) {
     unit = x / a.nsq;
-    run_quant<NG, EXTRA>(a, unit, x % a.nsq, sm);
+    if (WPC)
+      run_quant_wpc<NG, EXTRA>(a, unit, x % a.nsq, *reinterpret_cast<WpcSmem*>(smem), smrec);
+    else
+      run_quant<NG, EXTRA>(a, unit, x % a.nsq, sm);
   } else {
     x -= U * a.nsq;
     unit = x / 2;
-    run_resid<NG>(a, unit, x % 2, sm.rec);
+    run_resid<NG>(a, unit, x % 2, smrec);
   }
 #ifdef KVLC_TRACE
   __syncthreads();
@@ -826,6 +937,20 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   __syncthreads();
   DT_STAMP(2, gtimer() | (1ull << 63));  // top bit: this CTA ran the unit's combine
 #endif
+}
+
+template <int NG, int EXTRA>
+__global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const DecArgs a) {
+  __shared__ __align__(16) SplitSmem sm;
+  split_body<NG, EXTRA, false>(a, reinterpret_cast<unsigned char*>(&sm));
+}
+
+// 72 KB of dynamic shared memory per CTA: 3 CTAs per SM
+constexpr int WPC_MINB = 3;
+template <int NG, int EXTRA>
+__global__ void __launch_bounds__(THREADS, WPC_MINB) split_kernel_wpc(const DecArgs a) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  split_body<NG, EXTRA, true>(a, dsm);
 }
 
 // The LSE combine as its own launch (programmatic dependent of split_kernel), used when a
@@ -972,6 +1097,16 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
 }
 
 // ------------------------------------------------------------- host ----
+// Quantized splits warp per chunk (default) or warp per slice (KVLC_WPC=0, A/B).
+bool wpc_on() {
+  static const int v = [] {
+    const char* e = getenv("KVLC_WPC");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+int split_minb() { return wpc_on() ? WPC_MINB : KVLC_SPLIT_MINB; }
+
 struct Plan {
   int NG, U, nsq, cpc, nrec, corr_on;
   size_t done_off, corr_off, rec_off, total;
@@ -990,7 +1125,25 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     return e ? atoi(e) : 0;
   }();
   int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : cpc_env;
-  if (cpc == 0) {
+  if (cpc == 0 && wpc_on()) {
+    // warp per chunk: a split's 4 warps take every 4th chunk, so splits are sized in
+    // whole chunks per warp (balanced warps; the CTA waits for its slowest warp before
+    // merging).  About one wave of splits at WPC_MINB CTAs per SM, at most 52 records per
+    // unit, then equal splits rounded up to a multiple of 4 chunks.
+    const long long warps = 148LL * WPC_MINB * WARPS;
+    const long long chunks = (long long)p.U * std::max(span, 1);
+    // chunks per warp; multi-wave workloads keep splits short (the tail of the last wave)
+    long long cpw = std::min(6LL, std::max(2LL, (chunks + warps / 2) / warps));
+    long long nsq = (std::max(span, 1) + 4 * cpw - 1) / (4 * cpw);
+    static const int rec_cap = [] {
+      const char* e = getenv("KVLC_RECCAP");
+      return e ? atoi(e) : 52;
+    }();
+    nsq = std::max(1LL, std::min(nsq, (long long)rec_cap));
+    long long per = (std::max(span, 1) + nsq - 1) / nsq;
+    per = (per + 3) / 4 * 4;
+    cpc = (int)std::max(4LL, std::min(128LL, per));
+  } else if (cpc == 0) {
     // Per-CTA fixed cost (pipeline fill, q / B build, record merge, arrival) favours
     // long splits; the tail favours many.  Measured on configs 2-4
     // (tools/run_cpc3.sh, run_cpc4.sh): about 1.5 waves of splits at
@@ -998,7 +1151,7 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     // unit (the last CTA of a unit merges them all), then equal-length splits.
     // Configs 2 / 3 / 4: 7 -> 9 / 8 / 20 chunks, 49.2 -> 44.4 / 38.1 -> 34.8 / 55.6 -> 46.5 us.
     // Rounded (not ceiled) wave target: 64 chunks per unit get 8 x 8 rather than 6 x 10 + 4.
-    const long long slots = 148LL * KVLC_SPLIT_MINB;
+    const long long slots = 148LL * split_minb();
     const long long chunks = (long long)p.U * std::max(span, 1);
     long long t = std::max(8LL, (4 * chunks + 3 * slots) / (6 * slots));  // round(chunks / (1.5 slots))
     static const int rec_cap = [] {
@@ -1072,7 +1225,7 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     return e ? atoi(e) : 0;
   }();
   a.corr_split = corr_split_env ? corr_split_env
-                                : ((long long)p.U * (p.nsq + 1) > 148LL * KVLC_SPLIT_MINB ? 2 : 1);
+                                : ((long long)p.U * (p.nsq + 1) > 148LL * split_minb() ? 2 : 1);
   int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? a.corr_split * p.U : 0) : 0);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -1087,22 +1240,33 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = take_cache_write(s) ? 0 : 1;  // the predecessor wrote cache state: full wait
+  cfg.numAttrs = take_cache_write(c) ? 0 : 1;  // the cache was written since its last decode: full wait
   if (o && o->ev_begin) KVLC_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(o->ev_begin), s));
-  if (NG <= 4) {
-    KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a));
-  } else {
-    // precision passes for > 4 heads per group (see quant_chunk); KVLC_EXTRA overrides (tuning)
-    static const int extra = [] {
-      const char* e = getenv("KVLC_EXTRA");
-      return e ? atoi(e) & 3 : 3;
-    }();
-    switch (extra) {
-      case 0: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 0>, a)); break;
-      case 1: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 1>, a)); break;
-      case 2: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 2>, a)); break;
-      default: KVLC_CUDA(cudaLaunchKernelEx(&cfg, split_kernel<NG, 3>, a)); break;
+  // precision passes for > 4 heads per group (see quant_chunk); KVLC_EXTRA overrides (tuning)
+  static const int extra_env = [] {
+    const char* e = getenv("KVLC_EXTRA");
+    return e ? atoi(e) & 3 : 3;
+  }();
+  const int extra = NG <= 4 ? 0 : extra_env;
+  if (wpc_on()) {
+    static bool attr_set[4] = {false, false, false, false};
+    void (*kfn)(const DecArgs) = NG <= 4 || extra == 0 ? split_kernel_wpc<NG, 0>
+                                 : extra == 1            ? split_kernel_wpc<NG, NG <= 4 ? 0 : 1>
+                                 : extra == 2            ? split_kernel_wpc<NG, NG <= 4 ? 0 : 2>
+                                                         : split_kernel_wpc<NG, NG <= 4 ? 0 : 3>;
+    if (!attr_set[extra]) {
+      KVLC_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WPC_SMEM));
+      attr_set[extra] = true;
     }
+    cfg.dynamicSmemBytes = WPC_SMEM;
+    KVLC_CUDA(cudaLaunchKernelEx(&cfg, kfn, a));
+    cfg.dynamicSmemBytes = 0;
+  } else {
+    void (*kfn)(const DecArgs) = NG <= 4 || extra == 0 ? split_kernel<NG, 0>
+                                 : extra == 1            ? split_kernel<NG, NG <= 4 ? 0 : 1>
+                                 : extra == 2            ? split_kernel<NG, NG <= 4 ? 0 : 2>
+                                                         : split_kernel<NG, NG <= 4 ? 0 : 3>;
+    KVLC_CUDA(cudaLaunchKernelEx(&cfg, kfn, a));
   }
   if (a.sep_combine) {
     cfg.gridDim = dim3(c->B * c->Hq);

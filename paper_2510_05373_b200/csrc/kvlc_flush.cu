@@ -1339,6 +1339,7 @@ int kvlc_prefill(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k,
   KVLC_REQUIRE(c->B <= MAX_B, "batch %d exceeds the supported %d sequences", c->B, MAX_B);
   cudaStream_t s = as_stream(stream);
   const int units = c->B * c->Hkv;
+  kvlc::note_cache_write(c);  // codes and chunk counts change: the next decode waits fully
   static thread_local SeqInfo seq;
   memset(&seq, 0, sizeof(seq));
   int max_nf = 0;
@@ -1418,7 +1419,7 @@ int kvlc_append(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k_t
   // a flush writes codes / chunk counts, which the next decode reads before its
   // griddepcontrol.wait: that decode must not overlap (a plain append only moves the
   // residual ring, read after the wait)
-  if (any_flush) kvlc::note_cache_write(stream);
+  if (any_flush) kvlc::note_cache_write(c);
   const int units = c->B * c->Hkv;
   append_kernel<<<units, D, 0, s>>>(*c, k_t, v_t, seq);
   if ((rc = check_launch("append"))) return rc;
@@ -1483,10 +1484,10 @@ int kvlc_serialize_unit(const kvlc_cache* c, int32_t unit, int32_t n_chunks, int
 
 int kvlc_deserialize_unit(const kvlc_cache* c, int32_t unit, const uint8_t* image, int32_t n_chunks,
                           int32_t res_len, int32_t rank, void* stream) {
-  kvlc::note_cache_write(stream);  // no PDL overlap for the next decode on this stream
   KVLC_NEED_DEVICE();
   int rc = check_cache(c);
   if (rc) return rc;
+  kvlc::note_cache_write(c);  // no PDL overlap for the next decode of this cache
   KVLC_REQUIRE(unit >= 0 && unit < c->B * c->Hkv, "unit %d out of range", unit);
   KVLC_REQUIRE(n_chunks >= 0 && n_chunks <= c->max_chunks, "cache of %d chunks exceeds capacity of %d chunks",
                n_chunks, c->max_chunks);

@@ -423,7 +423,6 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
   st.init();
   const int lo = a.chunk_lo + split * a.cpc;
   const int cap_hi = min(min(a.chunk_hi, c.max_chunks), lo + a.cpc);  // no memory read
-  const int n_ch = min(c.n_chunks[b], a.chunk_hi);                      // in flight meanwhile
   const size_t cb0 = (size_t)unit * c.max_chunks;
   QuantSmem& q = sm.quant;
   if (threadIdx.x < 2 * NBUF) qb_init(threadIdx.x < NBUF ? &q.full[threadIdx.x] : &q.empty[threadIdx.x - NBUF], WARPS);
@@ -440,25 +439,28 @@ __device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) 
     for (int s = 0; s < n_pro; ++s) issue_chunk(c, cb0 + lo + s, q.stage[s], &q.sfull[s]);
   }
   __syncthreads();  // barriers initialised before any warp waits or arrives
+  // the chunk count and q may come from a programmatic-launch predecessor (a flush,
+  // kvlc_stage_input): both are read after the wait, their loads issued together
+  griddep_wait();
+  const int n_ch = min(c.n_chunks[b], a.chunk_hi);
+  // q (fp16, exact from bf16) for this warp's B share: column n = g,
+  // channels 32w + 16e + 2t + {0,1} (+8)
+  uint32_t raw[4];
+  {
+    const int head = HILO ? (g >> 1) : g;
+    const bool valid = head < NG;
+    const uint32_t* qp = reinterpret_cast<const uint32_t*>(
+        a.q + ((size_t)b * c.Hq + (size_t)kvh * NG + (valid ? head : 0)) * D);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) raw[i] = valid ? __ldg(qp + 16 * warp + 8 * (i >> 1) + t + 4 * (i & 1)) : 0u;
+  }
   const int hi = min(n_ch, lo + a.cpc);
   const int n = max(0, hi - lo);
   if (n > 0) {
-    // q (fp16, exact from bf16) for this warp's B share: column n = g,
-    // channels 32w + 16e + 2t + {0,1} (+8)
     uint32_t qs[4];
-    griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
-    {
-      const int head = HILO ? (g >> 1) : g;
-      const bool valid = head < NG;
-      const uint32_t* qp = reinterpret_cast<const uint32_t*>(
-          a.q + ((size_t)b * c.Hq + (size_t)kvh * NG + (valid ? head : 0)) * D);
-      uint32_t raw[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) raw[i] = valid ? __ldg(qp + 16 * warp + 8 * (i >> 1) + t + 4 * (i & 1)) : 0u;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        qs[i] = h2u(__floats2half2_rn(__uint_as_float(raw[i] << 16), __uint_as_float(raw[i] & 0xffff0000u)));
-    }
+    for (int i = 0; i < 4; ++i)
+      qs[i] = h2u(__floats2half2_rn(__uint_as_float(raw[i] << 16), __uint_as_float(raw[i] & 0xffff0000u)));
     tc::mbar_wait(&q.sfull[0], 0u);
 #ifndef KVLC_PROBE_NOMATH  // probe build: the stream and barriers without the math (timing only)
     build_b<NG>(q, 0, q.stage[0], qs, warp, lane);
