@@ -114,7 +114,35 @@ struct DecArgs {
   void* out;              // [B][Hq][D] bf16 / f32 (final output)
   float* rec_out;         // partial mode: [B][Hq][PREC] (split-KV across devices)
   int sep_combine;        // 1: the combine is combine_kernel, PDL-chained (no arrival counters)
+  uint32_t* queue;        // persistent split grid: task counter (zero between launches), or null
+  int ntask;              // tasks of the split grid
 };
+
+#ifdef KVLC_TRACE
+// per-CTA timeline (tools/trace_decode.py): globaltimer at entry, before the arrival
+// atomic and at exit, task kind (0 correction, 1 split, 2 residual), SM id
+constexpr int DT_MAX = 8192;
+__device__ unsigned long long g_dtrace[DT_MAX][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
+#define DT_STAMP(i, v) \
+  do { if (threadIdx.x == 0 && blockIdx.x < DT_MAX) g_dtrace[blockIdx.x][i] = (v); } while (0)
+// phase stamps inside a task (tools/trace_decode.py prints them per task kind)
+__device__ unsigned long long g_dphase[DT_MAX][4];
+#define PH_STAMP(i) \
+  do { if (threadIdx.x == 0 && blockIdx.x < DT_MAX) g_dphase[blockIdx.x][i] = gtimer(); } while (0)
+#else
+#define PH_STAMP(i) do { } while (0)
+#define DT_STAMP(i, v) do { } while (0)
+#endif
 
 #include "kvlc_quant.cuh"
 #include "kvlc_quant_wpc.cuh"
@@ -125,7 +153,7 @@ __device__ __forceinline__ int res_sigma(int r) {  // QK row -> slot offset with
 }
 
 template <int NG>
-__device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
+__device__ __forceinline__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
   const kvlc_cache& c = a.c;
   constexpr bool HILO = NG <= 4;
   constexpr int NH = WarpState<NG>::NH;
@@ -248,7 +276,7 @@ __device__ void run_resid(const DecArgs& a, int unit, int hf, float* smrec) {
 // 128 rows of S (8 / 4 rows per warp per pass, lanes across the 256 features).  These
 // CTAs come first in the grid, so their S stream overlaps the code stream.
 template <int NG>
-__device__ void run_corr_unit(const DecArgs& a, int unit, float* smf) {
+__device__ __forceinline__ void run_corr_unit(const DecArgs& a, int unit, float* smf) {
   static_assert(HALF == THREADS, "one feature of each half per thread");
   const kvlc_cache& c = a.c;
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
@@ -431,7 +459,7 @@ __device__ __forceinline__ void corr_half_dots(const DecArgs& a, int unit, int h
   }
   // C_n partial = S[:, h] phi_h (attention.py:227): per pass a warp takes RPW rows; per-lane
   // partial dots, then one reduce-scatter per 32 values (lane L ends with value L's total)
-  constexpr int RPW = NG > 4 ? 4 : 8;  // rows per warp per pass (register budget at 8 heads)
+  constexpr int RPW = NG > 4 ? 8 : 16;  // rows per warp per pass (register budget at 8 heads)
   constexpr int NV = RPW * NG;
   constexpr int NB = (NV + 31) / 32;
 #pragma unroll 1
@@ -478,25 +506,37 @@ __device__ __forceinline__ void corr_half_dots(const DecArgs& a, int unit, int h
 
 // Correction of one unit, feature half h (attention.py:224-231): phi_q of the unit's NG
 // query heads over half h (feature_map, adapter.py:80-88: the softmax is per half, so the
-// halves are independent; thread t owns feature t, W_h columns read from L2 KVLC_PHI_BATCH
-// channels per round trip), then the half's partial C_d = P_h . phi_h and C_n = S[:, h] phi_h
-// (RPW rows per warp per pass, lanes across the 128 features, one reduce-scatter per 32
-// values).  Two CTAs per unit halve the longest task of the grid (a whole-unit CTA ran
-// ~18 us against ~14 us splits and set the tail, tools/trace_decode.py); the combine adds
-// the halves.  These CTAs come first in the grid, so their S stream overlaps the codes.
+// halves are independent), then the half's partial C_d = P_h . phi_h and C_n = S[:, h] phi_h.
+// Latency, not work, sets these CTAs' time (r02 traces: ~10 us, S and W load rounds), so:
+//   * the half's S columns are prefetched into L2 at CTA start (one 512-B bulk prefetch per
+//     row), before the predecessor grid is waited for;
+//   * z = q W_h splits the channels over the warps (warp w: channels 32w..32w+31, lane l:
+//     features 4l..4l+3, 16-B loads of W rows, two rounds of 16 in flight instead of four
+//     rounds of 32 scalar loads), the 4 warps' partial sums meet in shared memory;
+//   * C_n takes two passes of 16 rows per warp (groups of <= 4 heads).
+// Two CTAs per unit halve the longest task of the grid; the combine adds the halves.  These
+// CTAs come first in the grid, so their S stream overlaps the codes.
 template <int NG>
-__device__ void run_corr(const DecArgs& a, int unit, int h, float* smf) {
+__device__ __forceinline__ void run_corr(const DecArgs& a, int unit, int h, float* smf) {
   static_assert(HALF == THREADS, "one feature of the half per thread");
   const kvlc_cache& c = a.c;
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const size_t qh0 = (size_t)b * c.Hq + (size_t)kvh * NG;
   float* corr = a.corr + (size_t)h * a.corr_half;
-  float* qs = smf;                 // [NG][D]
-  float* phs = qs + NG * D;        // [NG][HALF]
-  float* red = phs + NG * HALF;    // [WARPS][NG]
-  float* stat = red + WARPS * NG;  // [NG]
+  float* qs = smf;                      // [NG][D]
+  float* part = qs + NG * D;            // [WARPS][NG][HALF] partial z, then phs [NG][HALF]
+  float* red = part + WARPS * NG * HALF;  // [WARPS][NG]
+  float* stat = red + WARPS * NG;       // [NG]
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;\n" ::"l"(c.S + ((size_t)unit * D + t) * RANK + h * HALF)
+               : "memory");
+  const float4* W = reinterpret_cast<const float4*>((h ? a.w2q : a.w1q) + ((size_t)kvh * D + 32 * warp) * HALF) + lane;
+  constexpr int PB = 16;  // W rows (16-B loads) in flight per thread
+  float4 w[PB];
+#pragma unroll
+  for (int k = 0; k < PB; ++k) w[k] = __ldg(W + k * (HALF / 4));  // L2-resident: before the wait
   griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
+  PH_STAMP(0);
   {  // all NG loads in flight before the shared-memory stores
     uint16_t qv[NG];
 #pragma unroll
@@ -505,158 +545,75 @@ __device__ void run_corr(const DecArgs& a, int unit, int h, float* smf) {
     for (int i = 0; i < NG; ++i) qs[i * D + t] = bf2f(qv[i]);
   }
   __syncthreads();
-  float z[NG];
+  PH_STAMP(1);
+  float z[NG][4];
 #pragma unroll
-  for (int i = 0; i < NG; ++i) z[i] = 0.f;
-  const float* W = (h ? a.w2q : a.w1q) + (size_t)kvh * D * HALF + t;
-#ifndef KVLC_PHI_BATCH
-#define KVLC_PHI_BATCH 32
-#endif
-  constexpr int PB = KVLC_PHI_BATCH;  // channels of W loads in flight per thread (16: +0.1 us, same registers)
-#pragma unroll 1
-  for (int c0 = 0; c0 < D; c0 += PB) {
-    float w[PB];
+  for (int i = 0; i < NG; ++i) z[i][0] = z[i][1] = z[i][2] = z[i][3] = 0.f;
 #pragma unroll
-    for (int k = 0; k < PB; ++k) w[k] = __ldg(W + (size_t)(c0 + k) * HALF);
+  for (int r = 0; r < 32 / PB; ++r) {
 #pragma unroll
-    for (int k = 0; k < PB; k += 4) {
+    for (int k = 0; k < PB; ++k) {
+      const int ch = 32 * warp + PB * r + k;
 #pragma unroll
       for (int i = 0; i < NG; ++i) {
-        const float4 x = *reinterpret_cast<const float4*>(qs + i * D + c0 + k);
-        z[i] = fmaf(x.x, w[k], z[i]);
-        z[i] = fmaf(x.y, w[k + 1], z[i]);
-        z[i] = fmaf(x.z, w[k + 2], z[i]);
-        z[i] = fmaf(x.w, w[k + 3], z[i]);
+        const float x = qs[i * D + ch];
+        z[i][0] = fmaf(x, w[k].x, z[i][0]);
+        z[i][1] = fmaf(x, w[k].y, z[i][1]);
+        z[i][2] = fmaf(x, w[k].z, z[i][2]);
+        z[i][3] = fmaf(x, w[k].w, z[i][3]);
       }
     }
-  }
-  // max-shifted softmax of the half (linalg.py:38-47)
+    if (r + 1 < 32 / PB) {
 #pragma unroll
-  for (int i = 0; i < NG; ++i) {
-    const float m = warp_max(z[i]);
-    if (lane == 0) red[warp * NG + i] = m;
-  }
-  __syncthreads();
-  if (t < NG) {
-    float m = red[t];
-#pragma unroll
-    for (int w = 1; w < WARPS; ++w) m = fmaxf(m, red[w * NG + t]);
-    stat[t] = m;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < NG; ++i) z[i] = expf(z[i] - stat[i]);
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < NG; ++i) {
-    const float sm_ = warp_sum(z[i]);
-    if (lane == 0) red[warp * NG + i] = sm_;
-  }
-  __syncthreads();
-  if (t < NG) {
-    float sm_ = 0.f;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) sm_ += red[w * NG + t];
-    stat[t] = sm_;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < NG; ++i) phs[i * HALF + t] = z[i] / stat[i];
-  __syncthreads();
-
-  corr_half_dots<NG>(a, unit, h, phs, corr, qh0, warp, lane);
-}
-
-// Correction half h with the weights staged by TMA (warp-per-chunk kernel: its CTAs hold
-// 72 KB of dynamic shared memory): W_h (64 KB, L2-resident, shared by the batch) lands in
-// shared memory in one round trip instead of 128 / KVLC_PHI_BATCH dependent L2 load
-// rounds, and the half's S columns are prefetched into L2 at CTA start so the C_n pass
-// reads them from L2 (the whole-CTA time was ~10 us of load latency, r02 trace).
-template <int NG>
-__device__ void run_corr_staged(const DecArgs& a, int unit, int h, unsigned char* smem) {
-  static_assert(HALF == THREADS, "one feature of the half per thread");
-  const kvlc_cache& c = a.c;
-  const int b = unit / c.Hkv, kvh = unit % c.Hkv;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const size_t qh0 = (size_t)b * c.Hq + (size_t)kvh * NG;
-  float* corr = a.corr + (size_t)h * a.corr_half;
-  float* Ws = reinterpret_cast<float*>(smem);  // [D][HALF] W_h, then phs [NG][HALF]
-  float* qs = Ws + D * HALF;                    // [NG][D]
-  float* red = qs + NG * D;                     // [WARPS][NG]
-  float* stat = red + WARPS * NG;               // [NG]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(stat + 8);
-  const float* Wg = (h ? a.w2q : a.w1q) + (size_t)kvh * D * HALF;
-  if (t == 0) {
-    tc::mbar_init(bar, 1);
-    tc::mbar_fence_init();
-    tc::mbar_expect_tx(bar, (uint32_t)(D * HALF * sizeof(float)));
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-      tc::bulk_g2s(Ws + p * (D * HALF / 4), Wg + p * (D * HALF / 4), (uint32_t)(D * HALF), bar);
-  }
-  // row t of the half's S columns (512 B) into L2 while phi_q is computed
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;\n" ::"l"(c.S + ((size_t)unit * D + t) * RANK + h * HALF)
-               : "memory");
-  griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
-  {
-    uint16_t qv[NG];
-#pragma unroll
-    for (int i = 0; i < NG; ++i) qv[i] = __ldg(a.q + (qh0 + i) * D + t);
-#pragma unroll
-    for (int i = 0; i < NG; ++i) qs[i * D + t] = bf2f(qv[i]);
-  }
-  __syncthreads();  // q in shared memory, barrier initialised
-  tc::mbar_wait(bar, 0u);
-  float z[NG];
-#pragma unroll
-  for (int i = 0; i < NG; ++i) z[i] = 0.f;
-#pragma unroll 4
-  for (int c0 = 0; c0 < D; c0 += 4) {
-    const float w0 = Ws[(c0 + 0) * HALF + t], w1 = Ws[(c0 + 1) * HALF + t];
-    const float w2 = Ws[(c0 + 2) * HALF + t], w3 = Ws[(c0 + 3) * HALF + t];
-#pragma unroll
-    for (int i = 0; i < NG; ++i) {
-      const float4 x = *reinterpret_cast<const float4*>(qs + i * D + c0);
-      z[i] = fmaf(x.x, w0, z[i]);
-      z[i] = fmaf(x.y, w1, z[i]);
-      z[i] = fmaf(x.z, w2, z[i]);
-      z[i] = fmaf(x.w, w3, z[i]);
+      for (int k = 0; k < PB; ++k) w[k] = __ldg(W + (PB * (r + 1) + k) * (HALF / 4));
     }
   }
+#pragma unroll
+  for (int i = 0; i < NG; ++i)
+    *reinterpret_cast<float4*>(part + (warp * NG + i) * HALF + 4 * lane) = make_float4(z[i][0], z[i][1], z[i][2], z[i][3]);
+  __syncthreads();
+  float zf[NG];
+#pragma unroll
+  for (int i = 0; i < NG; ++i) {
+    zf[i] = part[i * HALF + t];
+#pragma unroll
+    for (int w2 = 1; w2 < WARPS; ++w2) zf[i] += part[(w2 * NG + i) * HALF + t];
+  }
   // max-shifted softmax of the half (linalg.py:38-47)
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    const float m = warp_max(z[i]);
+    const float m = warp_max(zf[i]);
     if (lane == 0) red[warp * NG + i] = m;
   }
-  __syncthreads();  // also: every thread is done with W_h (phs reuses its space)
+  __syncthreads();
   if (t < NG) {
     float m = red[t];
 #pragma unroll
-    for (int w = 1; w < WARPS; ++w) m = fmaxf(m, red[w * NG + t]);
+    for (int w2 = 1; w2 < WARPS; ++w2) m = fmaxf(m, red[w2 * NG + t]);
     stat[t] = m;
   }
   __syncthreads();
 #pragma unroll
-  for (int i = 0; i < NG; ++i) z[i] = expf(z[i] - stat[i]);
+  for (int i = 0; i < NG; ++i) zf[i] = expf(zf[i] - stat[i]);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < NG; ++i) {
-    const float sm_ = warp_sum(z[i]);
+    const float sm_ = warp_sum(zf[i]);
     if (lane == 0) red[warp * NG + i] = sm_;
   }
   __syncthreads();
   if (t < NG) {
     float sm_ = 0.f;
 #pragma unroll
-    for (int w = 0; w < WARPS; ++w) sm_ += red[w * NG + t];
+    for (int w2 = 0; w2 < WARPS; ++w2) sm_ += red[w2 * NG + t];
     stat[t] = sm_;
   }
   __syncthreads();
-  float* phs = Ws;
+  float* phs = part;  // every thread has read its partial sums (barriers above)
 #pragma unroll
-  for (int i = 0; i < NG; ++i) phs[i * HALF + t] = z[i] / stat[i];
+  for (int i = 0; i < NG; ++i) phs[i * HALF + t] = zf[i] / stat[i];
   __syncthreads();
+  PH_STAMP(2);
   corr_half_dots<NG>(a, unit, h, phs, corr, qh0, warp, lane);
 }
 
@@ -847,49 +804,24 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
 // task: quantized splits, residual halves, correction rows.  Every CTA bumps
 // its unit's arrival counter after publishing its record; the last one
 // performs the LSE combine of the unit (no separate combine launch).
-#ifdef KVLC_TRACE
-// per-CTA timeline (tools/trace_decode.py): globaltimer at entry, before the arrival
-// atomic and at exit, task kind (0 correction, 1 split, 2 residual), SM id
-constexpr int DT_MAX = 8192;
-__device__ unsigned long long g_dtrace[DT_MAX][4];
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ uint32_t smid() {
-  uint32_t s;
-  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
-  return s;
-}
-#define DT_STAMP(i, v) \
-  do { if (threadIdx.x == 0 && blockIdx.x < DT_MAX) g_dtrace[blockIdx.x][i] = (v); } while (0)
-#else
-#define DT_STAMP(i, v) do { } while (0)
-#endif
 
 #ifndef KVLC_SPLIT_MINB
 #define KVLC_SPLIT_MINB 4
 #endif
 // WPC: quantized splits run warp per chunk (kvlc_quant_wpc.cuh, dynamic shared memory)
 // instead of warp per 32-token slice (kvlc_quant.cuh, static shared memory)
+// One task of the split grid: correction rows, a quantized split or a residual half.
 template <int NG, int EXTRA, bool WPC>
-__device__ __forceinline__ void split_body(const DecArgs& a, unsigned char* smem) {
+__device__ __forceinline__ int run_task(const DecArgs& a, unsigned char* smem, int x) {
   SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem);
   float* const smrec = reinterpret_cast<float*>(smem);
-  __shared__ int last;
   const int U = a.c.B * a.c.Hkv;
-  const int ncorr = a.tail && a.corr_on ? a.corr_split * U : 0;  // correction CTAs first (S overlaps codes)
-  int x = blockIdx.x, unit;
-#ifdef KVLC_TRACE
-  const unsigned long long t_enter = gtimer();
-#endif
+  const int ncorr = a.tail && a.corr_on ? a.corr_split * U : 0;  // correction tasks first (S overlaps codes)
+  int unit;
   if (x < ncorr) {
     unit = a.corr_split == 2 ? x >> 1 : x;
 #ifndef KVLC_PROBE_NOCORR  // probe build: correction CTAs exit at once (timing only)
-    if (a.corr_split == 2 && WPC)
-      run_corr_staged<NG>(a, unit, x & 1, smem);
-    else if (a.corr_split == 2)
+    if (a.corr_split == 2)
       run_corr<NG>(a, unit, x & 1, smrec);
     else
       run_corr_unit<NG>(a, unit, smrec);
@@ -904,6 +836,37 @@ __device__ __forceinline__ void split_body(const DecArgs& a, unsigned char* smem
     x -= U * a.nsq;
     unit = x / 2;
     run_resid<NG>(a, unit, x % 2, smrec);
+  }
+  return unit;
+}
+
+template <int NG, int EXTRA, bool WPC>
+__device__ __forceinline__ void split_body(const DecArgs& a, unsigned char* smem) {
+  __shared__ int last;
+  __shared__ int next;
+  const int U = a.c.B * a.c.Hkv;
+  const int ncorr = a.tail && a.corr_on ? a.corr_split * U : 0;
+  int x = blockIdx.x, unit;
+#ifdef KVLC_TRACE
+  const unsigned long long t_enter = gtimer();
+#endif
+  // One call site of run_task (inlined): with a task counter (persistent warp-per-chunk
+  // grid) the CTA runs task blockIdx.x first (its code stream may start before the
+  // predecessor grid completes), then tasks gridDim.x + (ticket of the counter) in order,
+  // so CTAs that finish early take the remaining splits and residual halves and no slot
+  // idles while another wave waits.  The last ticket resets the counter.
+  for (;;) {
+    unit = run_task<NG, EXTRA, WPC>(a, smem, x);
+    if (!WPC || a.queue == nullptr) break;
+    __syncthreads();  // every warp is done with the task's shared memory
+    if (threadIdx.x == 0) {
+      const uint32_t d = atomicAdd(a.queue, 1u);
+      if (d == (uint32_t)(a.ntask - 1)) *a.queue = 0u;
+      next = (int)d + gridDim.x;
+    }
+    __syncthreads();
+    x = next;
+    if (x >= a.ntask) break;
   }
 #ifdef KVLC_TRACE
   __syncthreads();
@@ -945,10 +908,11 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
   split_body<NG, EXTRA, false>(a, reinterpret_cast<unsigned char*>(&sm));
 }
 
-// 72 KB of dynamic shared memory per CTA: 3 CTAs per SM
-constexpr int WPC_MINB = 3;
+// 55 KB of dynamic shared memory per CTA: 4 CTAs per SM for groups of <= 4 heads (q in
+// shared memory, 128 registers), 3 for larger groups (q and the lo B parts in registers)
+constexpr int wpc_minb(int ng) { return ng <= 4 ? 4 : 3; }
 template <int NG, int EXTRA>
-__global__ void __launch_bounds__(THREADS, WPC_MINB) split_kernel_wpc(const DecArgs a) {
+__global__ void __launch_bounds__(THREADS, wpc_minb(NG)) split_kernel_wpc(const DecArgs a) {
   extern __shared__ __align__(128) unsigned char dsm[];
   split_body<NG, EXTRA, true>(a, dsm);
 }
@@ -1097,15 +1061,18 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
 }
 
 // ------------------------------------------------------------- host ----
-// Quantized splits warp per chunk (default) or warp per slice (KVLC_WPC=0, A/B).
-bool wpc_on() {
+// Quantized splits warp per chunk or warp per 32-token slice.  Same-box A/B (r02,
+// tools/run_var.sh): config 2 (4 heads per group) 37.0 vs 36.8 us, config 4 29.7 vs 33.5 us,
+// config 3 (7 heads: 150+ registers, 3 CTAs per SM) 26.9-28.8 vs 24.9 us; so warp per chunk
+// for groups of <= 4 heads.  KVLC_WPC=0 / 1 forces either (A/B).
+bool wpc_on(int ng) {
   static const int v = [] {
     const char* e = getenv("KVLC_WPC");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : -1;
   }();
-  return v != 0;
+  return v < 0 ? ng <= 4 : v != 0;
 }
-int split_minb() { return wpc_on() ? WPC_MINB : KVLC_SPLIT_MINB; }
+int split_minb(int ng) { return wpc_on(ng) ? wpc_minb(ng) : KVLC_SPLIT_MINB; }
 
 struct Plan {
   int NG, U, nsq, cpc, nrec, corr_on;
@@ -1125,12 +1092,12 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     return e ? atoi(e) : 0;
   }();
   int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : cpc_env;
-  if (cpc == 0 && wpc_on()) {
+  if (cpc == 0 && wpc_on(p.NG)) {
     // warp per chunk: a split's 4 warps take every 4th chunk, so splits are sized in
     // whole chunks per warp (balanced warps; the CTA waits for its slowest warp before
     // merging).  About one wave of splits at WPC_MINB CTAs per SM, at most 52 records per
     // unit, then equal splits rounded up to a multiple of 4 chunks.
-    const long long warps = 148LL * WPC_MINB * WARPS;
+    const long long warps = 148LL * wpc_minb(p.NG) * WARPS;
     const long long chunks = (long long)p.U * std::max(span, 1);
     // chunks per warp; multi-wave workloads keep splits short (the tail of the last wave)
     long long cpw = std::min(6LL, std::max(2LL, (chunks + warps / 2) / warps));
@@ -1151,7 +1118,7 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     // unit (the last CTA of a unit merges them all), then equal-length splits.
     // Configs 2 / 3 / 4: 7 -> 9 / 8 / 20 chunks, 49.2 -> 44.4 / 38.1 -> 34.8 / 55.6 -> 46.5 us.
     // Rounded (not ceiled) wave target: 64 chunks per unit get 8 x 8 rather than 6 x 10 + 4.
-    const long long slots = 148LL * split_minb();
+    const long long slots = 148LL * split_minb(p.NG);
     const long long chunks = (long long)p.U * std::max(span, 1);
     long long t = std::max(8LL, (4 * chunks + 3 * slots) / (6 * slots));  // round(chunks / (1.5 slots))
     static const int rec_cap = [] {
@@ -1172,7 +1139,7 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   // arrival counters first: their offset must not depend on the split plan
   // (they are zero-initialised once and left at zero by every launch)
   p.done_off = 0;
-  const size_t base = align_up((size_t)p.U * sizeof(uint32_t));
+  const size_t base = align_up((size_t)(p.U + 1) * sizeof(uint32_t));  // + the task counter
   p.corr_off += base;
   p.rec_off += base;
   p.total = p.rec_off + align_up((size_t)p.U * p.nrec * p.NG * REC * sizeof(float));
@@ -1225,8 +1192,22 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     return e ? atoi(e) : 0;
   }();
   a.corr_split = corr_split_env ? corr_split_env
-                                : ((long long)p.U * (p.nsq + 1) > 148LL * split_minb() ? 2 : 1);
+                                : ((long long)p.U * (p.nsq + 1) > 148LL * split_minb(NG) ? 2 : 1);
   int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? a.corr_split * p.U : 0) : 0);
+  // persistent split grid (warp-per-chunk kernel, separate combine): at most one wave of
+  // CTAs that take tasks from a counter.  Measured slower (config 2 split 37.0 -> 38.1 us
+  // same box, r02: every task keeps its start-up and record costs, and late long tasks
+  // stretch the tail), so off unless KVLC_DYN=1.
+  static const int dyn_env = [] {
+    const char* e = getenv("KVLC_DYN");
+    return e ? atoi(e) : 0;
+  }();
+  a.ntask = grid;
+  a.queue = nullptr;
+  if (wpc_on(NG) && a.sep_combine && dyn_env) {
+    a.queue = reinterpret_cast<uint32_t*>(ws + p.done_off) + p.U;
+    grid = std::min(grid, 148 * split_minb(NG));
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(THREADS);
@@ -1248,7 +1229,7 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     return e ? atoi(e) & 3 : 3;
   }();
   const int extra = NG <= 4 ? 0 : extra_env;
-  if (wpc_on()) {
+  if (wpc_on(NG)) {
     static bool attr_set[4] = {false, false, false, false};
     void (*kfn)(const DecArgs) = NG <= 4 || extra == 0 ? split_kernel_wpc<NG, 0>
                                  : extra == 1            ? split_kernel_wpc<NG, NG <= 4 ? 0 : 1>
@@ -1307,6 +1288,9 @@ bool adapter_active(const kvlc_adapter* ad) {
 using namespace kvlc;
 
 #ifdef KVLC_TRACE
+extern "C" int kvlc_dphase_copy(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, g_dphase, bytes < sizeof(g_dphase) ? bytes : sizeof(g_dphase)) == cudaSuccess ? 0 : 2;
+}
 extern "C" int kvlc_dtrace_copy(void* dst, size_t bytes) {
   return cudaMemcpyFromSymbol(dst, g_dtrace, bytes < sizeof(g_dtrace) ? bytes : sizeof(g_dtrace)) == cudaSuccess ? 0 : 2;
 }

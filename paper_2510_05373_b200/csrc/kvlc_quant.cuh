@@ -413,7 +413,7 @@ __device__ __forceinline__ void cta_merge(float* sm, float* out) {
 
 // A quantized split: chunks [lo, hi) of one unit.
 template <int NG, int EXTRA>
-__device__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) {
+__device__ __forceinline__ void run_quant(const DecArgs& a, int unit, int split, SplitSmem& sm) {
   const kvlc_cache& c = a.c;
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

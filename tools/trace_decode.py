@@ -55,3 +55,20 @@ print("exits per 2 us:", " ".join(str(x) for x in hist))
 act = [int(((start <= x) & (end > x)).sum()) for x in np.arange(0, end.max(), 2.0)]
 print("resident CTAs per 2 us:", " ".join(str(x) for x in act))
 np.save(os.path.join(ROOT, "gpurun_out", "dtrace.npy"), np.stack([start, work, end, kind, sm, comb], 1))
+# phase stamps (PH_STAMP): correction 0 after griddepcontrol.wait, 1 q staged, 2 phi done;
+# split 0 after the wait, 1 q staged, 2 chunks done; relative to the CTA start
+try:
+    fp = lib["kvlc_dphase_copy"]
+    fp.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    ph = np.zeros((8192, 4), np.uint64)
+    assert fp(ph.ctypes.data, ph.nbytes) == 0
+    ph = ph[:n].astype(np.int64)
+    for kd, name in enumerate(["correction", "split"]):
+        m = kind == kd
+        if not m.any():
+            continue
+        rel = (ph[m, :3] - t[m, 0:1]) / 1e3
+        print(f"{name:10s} phases (us from CTA start, mean / max): " +
+              "  ".join(f"p{k} {rel[:, k].mean():6.2f}/{rel[:, k].max():6.2f}" for k in range(3)))
+except (KeyError, AttributeError):
+    pass
