@@ -427,6 +427,23 @@ class BatchedKVCache:
         return dict(kwords=kw.cpu().numpy().view(np.uint32), vwords=vw.cpu().numpy().view(np.uint32),
                     kscale=m[0], kzero=m[1], vscale=m[2], vzero=m[3])
 
+    def export_unit(self, b: int, kvh: int, n_chunks: int | None = None) -> dict:
+        """Every quantized chunk of one unit in the reference layout, stacked on a leading
+        chunk axis (kvlc_export_chunk per chunk into device buffers, one host copy)."""
+        u = b * self.Hkv + kvh
+        n = int(self.n_chunks[b]) if n_chunks is None else n_chunks
+        dev = self.device
+        kw = torch.empty((n, 8, 128), dtype=torch.int32, device=dev)
+        vw = torch.empty((n, 128, 8), dtype=torch.int32, device=dev)
+        meta = torch.empty((n, 4, 128), dtype=torch.float16, device=dev)
+        for ci in range(n):
+            _lib.call("kvlc_export_chunk", ctypes.byref(self._struct), u, ci, _ptr(kw[ci]), _ptr(vw[ci]),
+                      _ptr(meta[ci, 0]), _ptr(meta[ci, 1]), _ptr(meta[ci, 2]), _ptr(meta[ci, 3]),
+                      _lib.stream_handle())
+        m = meta.cpu().numpy()
+        return dict(kwords=kw.cpu().numpy().view(np.uint32), vwords=vw.cpu().numpy().view(np.uint32),
+                    kscale=m[:, 0], kzero=m[:, 1], vscale=m[:, 2], vzero=m[:, 3])
+
     def residual(self, b: int, kvh: int):
         """Live residual window of one unit, oldest first, as float32 host arrays."""
         u = b * self.Hkv + kvh

@@ -43,6 +43,15 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 void note_cache_write(const kvlc_cache* c);  // kvlc_api.cu: the next decode of `c` waits fully
 bool take_cache_write(const kvlc_cache* c);  // true (and cleared) if `c` was marked
 
+// Fragment-native code words (kvlc_flush.cu pack_k_word / pack_v_word) are stored rotated
+// left by 2 bits: code (byte q, bit pair j) sits at bit (8 q + 2 j + 2) mod 32, so the
+// decode's fp16 operands (x & (0x000C000C << 2 j), and the same on x rotated right by 8)
+// are c 4^(j+1) 2^-24 rather than c 4^j 2^-24.  The smallest subnormals (c 2^-24) lost
+// low-order product bits in the tensor core (rows of j = 0 carried a -8e-6 bias in the
+// output at 131k tokens, 17x the j = 1 rows; tools/decode_err_diag.py).
+__device__ __forceinline__ uint32_t frag_store(uint32_t w) { return __funnelshift_l(w, w, 2); }
+__device__ __forceinline__ uint32_t frag_load(uint32_t w) { return __funnelshift_r(w, w, 2); }
+
 inline int lane_bits(int bits) { return bits == 2 ? 2 : (bits == 8 ? 8 : 4); }
 inline int lanes_per_word(int bits) { return 32 / lane_bits(bits); }
 inline bool valid_bits(int bits) { return bits == 2 || bits == 3 || bits == 4 || bits == 8; }

@@ -80,12 +80,14 @@ __device__ __forceinline__ uint4 ldg4(const void* p) {
 __device__ __forceinline__ uint2 ldg2(const void* p) {
   return __ldg(reinterpret_cast<const uint2*>(p));
 }
-// half2 of fp16 subnormals (c_lo * 4^j * 2^-24, c_hi * 4^j * 2^-24)
-__device__ __forceinline__ uint32_t code_h2(uint32_t x, int j) { return x & (0x00030003u << (2 * j)); }
+// half2 of fp16 subnormals (c_lo * 4^(j+1) * 2^-24, c_hi * 4^(j+1) * 2^-24) from a stored
+// (rotated, frag_store) word: bytes 0 / 2 of the unrotated word; code_hi(x) brings bytes 1 / 3
+__device__ __forceinline__ uint32_t code_h2(uint32_t x, int j) { return x & (0x000C000Cu << (2 * j)); }
+__device__ __forceinline__ uint32_t code_hi(uint32_t x) { return __funnelshift_r(x, x, 8); }
 
-// 2^24 * 4^-j
+// 2^24 * 4^-(j+1)
 __device__ __forceinline__ constexpr float code_unscale(int j) {
-  return j == 0 ? 16777216.f : (j == 1 ? 4194304.f : (j == 2 ? 1048576.f : 262144.f));
+  return j == 0 ? 4194304.f : (j == 1 ? 1048576.f : (j == 2 ? 262144.f : 65536.f));
 }
 
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
@@ -844,8 +846,6 @@ template <int NG, int EXTRA, bool WPC>
 __device__ __forceinline__ void split_body(const DecArgs& a, unsigned char* smem) {
   __shared__ int last;
   __shared__ int next;
-  const int U = a.c.B * a.c.Hkv;
-  const int ncorr = a.tail && a.corr_on ? a.corr_split * U : 0;
   int x = blockIdx.x, unit;
 #ifdef KVLC_TRACE
   const unsigned long long t_enter = gtimer();
@@ -872,7 +872,11 @@ __device__ __forceinline__ void split_body(const DecArgs& a, unsigned char* smem
   __syncthreads();
   DT_STAMP(0, t_enter);
   DT_STAMP(1, gtimer());
-  DT_STAMP(3, ((unsigned long long)smid() << 32) | (unsigned long long)((blockIdx.x < ncorr ? 0 : blockIdx.x < ncorr + U * a.nsq ? 1 : 2) << 24 | unit));
+  {
+    const int U = a.c.B * a.c.Hkv, ncorr = a.tail && a.corr_on ? a.corr_split * U : 0;
+    DT_STAMP(3, ((unsigned long long)smid() << 32) |
+                    (unsigned long long)((blockIdx.x < ncorr ? 0 : blockIdx.x < ncorr + U * a.nsq ? 1 : 2) << 24 | unit));
+  }
   if (a.sep_combine) DT_STAMP(2, gtimer());
 #endif
   if (a.sep_combine) {

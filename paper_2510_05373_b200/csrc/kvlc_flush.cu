@@ -87,13 +87,13 @@ __device__ __forceinline__ uint32_t pack_v_word(const uint8_t* codes, int wi) {
 __device__ __forceinline__ uint32_t k_code(const uint32_t* words, int t, int c) {
   const int w = t >> 5, u = t & 31, g = u >> 2, j = u & 3;
   const int kt = c >> 4, cc = c & 15, t0 = (cc & 7) >> 1, q = ((cc & 1) << 1) | (cc >> 3);
-  return (words[((w * 32) + 4 * g + t0) * 8 + kt] >> (8 * q + 2 * j)) & 3u;
+  return (frag_load(words[((w * 32) + 4 * g + t0) * 8 + kt]) >> (8 * q + 2 * j)) & 3u;
 }
 
 __device__ __forceinline__ uint32_t v_code(const uint32_t* words, int t, int c) {
   const int w = t >> 5, u = t & 31, t0 = u >> 3, hi = (u >> 2) & 1, mt = (u >> 1) & 1, lo = u & 1;
   const int q = lo + 2 * hi, g = c & 7, r = (c >> 3) & 1, mv = c >> 4, p = mv >> 1, j = 2 * (mv & 1) + r;
-  return (words[((w * 32) + 4 * g + t0) * 8 + 4 * mt + p] >> (8 * q + 2 * j)) & 3u;
+  return (frag_load(words[((w * 32) + 4 * g + t0) * 8 + 4 * mt + p]) >> (8 * q + 2 * j)) & 3u;
 }
 
 constexpr int MAX_B = 1024;
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs
     }
     __syncthreads();
     // pack the key codes into the decode kernel's fragment-native word layout
-    for (int wi = tid; wi < 1024; wi += FLUSH_THREADS) c.kcodes[cb * 1024 + wi] = pack_k_word(codes_s, wi);
+    for (int wi = tid; wi < 1024; wi += FLUSH_THREADS) c.kcodes[cb * 1024 + wi] = frag_store(pack_k_word(codes_s, wi));
     __syncthreads();
 
     // ---- K2: values, FWHT post-rotation (fp64) then token-wise quantization ----
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs
       }
     }
     __syncthreads();
-    for (int wi = tid; wi < 1024; wi += FLUSH_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word(codes_s, wi);
+    for (int wi = tid; wi < 1024; wi += FLUSH_THREADS) c.vcodes[cb * 1024 + wi] = frag_store(pack_v_word(codes_s, wi));
     __syncthreads();
     if (!a.use_adapter) continue;
 
@@ -552,14 +552,14 @@ __global__ void deserialize_unit_kernel(kvlc_cache c, int unit, int n, int n_res
       codes[i] = (uint8_t)((kw[(t >> 4) * 128 + ch] >> (2 * (t & 15))) & 3u);
     }
     __syncthreads();
-    for (int wi = tid; wi < 1024; wi += blockDim.x) c.kcodes[cb * 1024 + wi] = pack_k_word(codes, wi);
+    for (int wi = tid; wi < 1024; wi += blockDim.x) c.kcodes[cb * 1024 + wi] = frag_store(pack_k_word(codes, wi));
     __syncthreads();
     for (int i = tid; i < G * D; i += blockDim.x) {
       const int t = i / D, ch = i % D;
       codes[i] = (uint8_t)((vw[t * 8 + (ch >> 4)] >> (2 * (ch & 15))) & 3u);
     }
     __syncthreads();
-    for (int wi = tid; wi < 1024; wi += blockDim.x) c.vcodes[cb * 1024 + wi] = pack_v_word(codes, wi);
+    for (int wi = tid; wi < 1024; wi += blockDim.x) c.vcodes[cb * 1024 + wi] = frag_store(pack_v_word(codes, wi));
     const uint16_t* km = reinterpret_cast<const uint16_t*>(img + L.kmeta) + (size_t)bx * 2 * D;
     const uint16_t* vs = reinterpret_cast<const uint16_t*>(img + L.vscale) + (size_t)bx * G;
     const uint16_t* vz = reinterpret_cast<const uint16_t*>(img + L.vzero) + (size_t)bx * G;
@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       if (writer) {
         const int wt = lane >> 3, g = lane & 7;  // tokens 32 wt + 4 g + r
 #pragma unroll
-        for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = cw[t0];
+        for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = frag_store(cw[t0]);
       }
     }
     // ---- K2: values, FWHT post-rotation (fp32, guarded), token-wise quantization ----
@@ -864,15 +864,18 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         }
       }
       const float hsf = 0.08838834764831845f;
-      float mnf = INFINITY, mxf = -INFINITY;
+      // row min / max of the unnormalised transform (scaling by hsf > 0 keeps the order, so
+      // mnf = mnu * hsf is bit-identical to the min of the scaled values)
+      float mnu = INFINITY, mxu = -INFINITY;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
+        mnu = fminf(mnu, xf[e]);
+        mxu = fmaxf(mxu, xf[e]);
         xf[e] *= hsf;
-        mnf = fminf(mnf, xf[e]);
-        mxf = fmaxf(mxf, xf[e]);
       }
-      mnf = warp_min(mnf);
-      mxf = warp_max(mxf);
+      mnu = warp_min(mnu);
+      mxu = warp_max(mxu);
+      float mnf = mnu * hsf, mxf = mxu * hsf;
       // Fast path in fp32.  fp32 FWHT error: a few ulps of the token's largest magnitude
       // (ferr); a token is re-evaluated exactly when a quotient lies within qtol of a
       // rounding tie or its zero / scale lies near an fp16 rounding midpoint (the stored
@@ -893,7 +896,14 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         amb |= range > 0.f && fabsf(q - floorf(q) - 0.5f) < qtol;
         code[e] = range > 0.f ? (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f) : 0u;
       }
-      float vmn = mnf, vsc = scf;
+      // the state kernel's fp32 (s, z') of v_q = s code + z: from the unnormalised min / max in
+      // fp64, each rounded once.  fp32(1/sqrt(128)) is 1.7e-8 low and fp32(1/3) 3e-8 high, and
+      // z' = z + 3/2 s enters S as the same-signed rank-1 term sum_t z'_t Phi_t for every
+      // token: a fixed relative bias of the per-token (s, z') grew the S error ~ n / sqrt(n)
+      // (4.0e-6 at 8k, 1.9e-5 at 131k tokens, 97 % of it channel-constant; tools/s_error_diag.py)
+      const double hsd = 0.088388347648318440550;  // 1 / sqrt(128)
+      float vsc = (float)(((double)mxu - (double)mnu) * (hsd / 3.0));
+      float vmid = (float)(0.5 * ((double)mnu + (double)mxu) * hsd);
       uint16_t meta_s = __half_as_ushort(__float2half_rn(scf)), meta_z = __half_as_ushort(__float2half_rn(mnf));
       if (__any_sync(0xffffffffu, amb)) {
         // fp64 FWHT: agrees with the dense fp64 x @ H to an ulp
@@ -958,8 +968,8 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         }
 #pragma unroll
         for (int e = 0; e < 4; ++e) code[e] = code2(x[e], mn, scale, inv);
-        vmn = (float)mn;
         vsc = (float)scale;
+        vmid = (float)(mn + 1.5 * scale);
         meta_s = __half_as_ushort(__double2half(scale));
         meta_z = __half_as_ushort(__double2half(mn));
       }
@@ -978,7 +988,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         auto hc = [&](uint32_t cd) { return (uint32_t)__half_as_ushort(__float2half_rn(((float)cd - 1.5f) * cs)); };
         *reinterpret_cast<uint2*>(a.cimg + slot * FT_TILE + ft_off(4 * lane, t)) =
             make_uint2(hc(code[0]) | (hc(code[1]) << 16), hc(code[2]) | (hc(code[3]) << 16));
-        if (lane == 0) a.vsz[slot * G + t] = make_float2(vsc * __int_as_float((127 + e) << 23), fmaf(1.5f, vsc, vmn));
+        if (lane == 0) a.vsz[slot * G + t] = make_float2(vsc * __int_as_float((127 + e) << 23), vmid);
       }
       if (writer && lane == 0) {
         c.vscale[cb * G + t] = meta_s;
@@ -986,7 +996,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       }
     }
   __syncthreads();
-  for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = pack_v_word_sw(sm.codes, wi);
+  for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = frag_store(pack_v_word_sw(sm.codes, wi));
 }
 
 #ifdef KVLC_TRACE

@@ -26,6 +26,14 @@
 #endif
 constexpr int STAGES = KVLC_STAGES;
 constexpr float LAZY = 8.f;
+// The lo halves of the PV B operand (p s - hi, ~2^-11 p s) go into their own MMA column
+// scaled by PV_LO_SCALE and are unscaled in warp_store: with the fp16-subnormal code
+// operands (c 4^j 2^-24) the unscaled lo products sat at the bottom of the tensor core's
+// product range and lost low-order bits (KVLC_PV_LO_SCALE A/B, tools/decode_err_diag.py)
+#ifndef KVLC_PV_LO_SCALE
+#define KVLC_PV_LO_SCALE 1.f
+#endif
+constexpr float PV_LO_SCALE = KVLC_PV_LO_SCALE;
 #ifndef KVLC_BBUF
 #define KVLC_BBUF 3
 #endif
@@ -59,6 +67,40 @@ __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
+}
+
+// Centring of the PV accumulator.  mma.sync accumulates in fp32 rounding toward zero
+// (tools/microbench/mma_rounding.cu: +0.6 ulp added 1000 times to 1.0 leaves 1.0), and the
+// accumulated sum p s code is all-positive while the output is the small difference
+// sum p s code + sum p z (codes 0..3, z the row minimum): at 32k tokens the truncation
+// bias, magnified by that cancellation, reached 1.6e-3 of max|out| (T4 is 1e-3).  So
+// after each chunk the accumulator drops 3/2 sum p s (the codes become c - 3/2, zero
+// mean) and the zero term accumulates the row midpoint z' = z + 3/2 s instead of z:
+// both sums stay small and the truncation acts on small values.
+// ps: this lane's sum of p s of the chunk per column group e (heads t / 2t + e).
+template <int NG>
+__device__ __forceinline__ void centre_acc(WarpState<NG>& st, float (&ps)[WarpState<NG>::NH]) {
+  constexpr bool HILO = NG <= 4;
+  constexpr int NH = WarpState<NG>::NH;
+#pragma unroll
+  for (int e = 0; e < NH; ++e) {
+    ps[e] += __shfl_xor_sync(0xffffffffu, ps[e], 4);
+    ps[e] += __shfl_xor_sync(0xffffffffu, ps[e], 8);
+    ps[e] += __shfl_xor_sync(0xffffffffu, ps[e], 16);
+  }
+#pragma unroll
+  for (int mv = 0; mv < 8; ++mv)
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      // row factor 4^j 2^-24 of the fp16-subnormal codes, j = 2 (mv & 1) + rr
+      const float f = -1.5f / code_unscale(2 * (mv & 1) + rr);
+      if (HILO) {
+        st.acc[mv][2 * rr] = fmaf(f, ps[0], st.acc[mv][2 * rr]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) st.acc[mv][2 * rr + e] = fmaf(f, ps[e], st.acc[mv][2 * rr + e]);
+      }
+    }
 }
 
 // One chunk of one unit in shared memory: the bytes of the global layouts.
@@ -194,7 +236,7 @@ __device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSm
       if (QK_LO) bl = sm.bl[buf][p][lane];
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const uint32_t x = kw[2 * p + e], y = x >> 8;
+        const uint32_t x = kw[2 * p + e], y = code_hi(x);
         const uint32_t b0 = e ? b.z : b.x, b1 = e ? b.w : b.y;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
@@ -271,19 +313,27 @@ __device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSm
   const float2 z01 = __half22float2(u2h(vz.x)), z23 = __half22float2(u2h(vz.y));
   const float svs[4] = {s01.x, s01.y, s23.x, s23.y}, svz[4] = {z01.x, z01.y, z23.x, z23.y};
   uint32_t bp[2][2], bpl[2][2];
+  float ps[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) ps[e] = 0.f;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const float sv = svs[2 * mt + r], zv = svz[2 * mt + r];
+      const float sv = svs[2 * mt + r], zv = fmaf(1.5f, svs[2 * mt + r], svz[2 * mt + r]);  // z' (centre_acc)
       if (HILO) {
         const float p = fast_exp2(cq[mt][2 * r] - st.m[0]);
         st.l[0] += p;
         st.z[0] = fmaf(p, zv, st.z[0]);
         const float pv = p * sv;
+        ps[0] += pv;
         // hi: pv truncated to 11 significant bits (fp16-exact), lo: the exact remainder
+        #ifdef KVLC_HI_RN
+        const float hi = __half2float(__float2half_rn(pv));
+#else
         const float hi = __uint_as_float(__float_as_uint(pv) & 0xffffe000u);
-        bp[mt][r] = movm_t(h2u(__floats2half2_rn(hi, pv - hi)));
+#endif
+        bp[mt][r] = movm_t(h2u(__floats2half2_rn(hi, (pv - hi) * PV_LO_SCALE)));
       } else {
         const float p0 = fast_exp2(cq[mt][2 * r] - st.m[0]);
         const float p1 = fast_exp2(cq[mt][2 * r + 1] - st.m[1]);
@@ -297,6 +347,12 @@ __device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSm
         if (PV_LO) {
           const float2 hf = __half22float2(hh);
           bpl[mt][r] = movm_t(h2u(__floats2half2_rn(a0 - hf.x, a1 - hf.y)));
+          ps[0] += a0;
+          ps[1] += a1;
+        } else {  // the MMA sees fp16(p s) only
+          const float2 hf = __half22float2(hh);
+          ps[0] += hf.x;
+          ps[1] += hf.y;
         }
       }
     }
@@ -309,7 +365,7 @@ __device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSm
   for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      const uint32_t x = vw[4 * mt + p], y = x >> 8;
+      const uint32_t x = vw[4 * mt + p], y = code_hi(x);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int mv = 2 * p + h;
@@ -320,6 +376,7 @@ __device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSm
       }
     }
   }
+  centre_acc<NG>(st, ps);
 }
 
 // Writes this warp's record (m_ref, l, m_true, -, y[c]) per head into shared memory.
@@ -355,7 +412,9 @@ __device__ __forceinline__ void warp_store(WarpState<NG>& st, float* smrec, int 
     for (int mv = 0; mv < 8; ++mv) {
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
-        float v = HILO ? st.acc[mv][2 * rr] + st.acc[mv][2 * rr + 1] : st.acc[mv][2 * rr + e];
+        float v = HILO ? (QUANT ? fmaf(st.acc[mv][2 * rr + 1], 1.f / PV_LO_SCALE, st.acc[mv][2 * rr])
+                                : st.acc[mv][2 * rr] + st.acc[mv][2 * rr + 1])
+                       : st.acc[mv][2 * rr + e];
         if (QUANT) v = fmaf(v, code_unscale(2 * (mv & 1) + rr), st.z[e]);
         r[4 + 16 * mv + g + 8 * rr] = v;
       }

@@ -130,7 +130,7 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
     const uint32_t kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
     for (int kt = 0; kt < 8; ++kt) {
-      const uint32_t x = kw[kt], y = x >> 8;
+      const uint32_t x = kw[kt], y = code_hi(x);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const uint32_t a0 = code_h2(x, 2 * mt), a1 = code_h2(x, 2 * mt + 1);
@@ -205,6 +205,9 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
 
   // ---- p (value scale folded in) as PV B fragments, then P V per slice ----
   tc::mbar_wait(vbar, vpar);
+  float ps[NH];
+#pragma unroll
+  for (int e = 0; e < NH; ++e) ps[e] = 0.f;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     const uint2 vs = reinterpret_cast<const uint2*>(vst.s + 32 * s)[g];
@@ -217,15 +220,20 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
     for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        const float sv = svs[2 * mt + r], zv = svz[2 * mt + r];
+        const float sv = svs[2 * mt + r], zv = fmaf(1.5f, svs[2 * mt + r], svz[2 * mt + r]);  // z' (centre_acc)
         if (HILO) {
           const float p = fast_exp2(cq[s][mt][2 * r] - st.m[0]);
           st.l[0] += p;
           st.z[0] = fmaf(p, zv, st.z[0]);
           const float pv = p * sv;
+          ps[0] += pv;
           // hi: pv truncated to 11 significant bits (fp16-exact), lo: the exact remainder
+          #ifdef KVLC_HI_RN
+          const float hi = __half2float(__float2half_rn(pv));
+#else
           const float hi = __uint_as_float(__float_as_uint(pv) & 0xffffe000u);
-          bp[mt][r] = movm_t(h2u(__floats2half2_rn(hi, pv - hi)));
+#endif
+          bp[mt][r] = movm_t(h2u(__floats2half2_rn(hi, (pv - hi) * PV_LO_SCALE)));
         } else {
           const float p0 = fast_exp2(cq[s][mt][2 * r] - st.m[0]);
           const float p1 = fast_exp2(cq[s][mt][2 * r + 1] - st.m[1]);
@@ -239,6 +247,12 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
           if (PV_LO) {
             const float2 hf = __half22float2(hh);
             bpl[mt][r] = movm_t(h2u(__floats2half2_rn(a0 - hf.x, a1 - hf.y)));
+            ps[0] += a0;
+            ps[1] += a1;
+          } else {  // the MMA sees fp16(p s) only
+            const float2 hf = __half22float2(hh);
+            ps[0] += hf.x;
+            ps[1] += hf.y;
           }
         }
       }
@@ -249,7 +263,7 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
     for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
-        const uint32_t x = vw[4 * mt + p], y = x >> 8;
+        const uint32_t x = vw[4 * mt + p], y = code_hi(x);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int mv = 2 * p + h;
@@ -261,6 +275,7 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
       }
     }
   }
+  centre_acc<NG>(st, ps);
 }
 
 // A quantized split, warp per chunk: chunks [lo, hi) of one unit, warp w takes lo + w + 4i.

@@ -1,10 +1,20 @@
-"""Parity at the BASELINE sizes (configs 2, 3 and 4) on sampled units.
+"""Parity at the BASELINE sizes (configs 2, 3 and 4) on sampled units, every chunk.
 
 The whole batch is prefilled and decoded on the GPU at full size; a seeded
-sample of (b, kv-head) units is rebuilt by the oracle (a unit is independent of
-the others) and compared: T1 code words and T2 fp16 metadata of
-sampled chunks bit-exact, T3 S / P, T4 decode output of the unit's query heads.
+sample of (b, kv-head) units (8 per config, all 4 at B1 x 4k) is rebuilt by the
+oracle in parallel host processes (a unit is independent of the others, SURVEY
+§8e) and compared at the survey's bounds:
+  T1  code words of EVERY chunk of each sampled unit bit-exact (reference layout),
+  T2  fp16 key / value scale and zero of every chunk equal float16(fp64 value),
+  T3  S and P within relative Frobenius 1e-5 of the fp64 reference,
+  T4  decode output of the unit's query heads within 1e-3 * max|ref| of
+      decode_step_blocked on the fp16-metadata reference cache.
+Configs: 2 = Llama-3-8B B16 x 8k; 3 = Qwen2.5-7B (28 q / 4 kv heads) at B1 x 4k,
+B16 x 8k and B64 x 32k (the largest single-GPU point of SURVEY §8(d)); 4 =
+Llama-3-8B B1 x 128k (131072 tokens, 1023 chunks).
 """
+import multiprocessing as mp
+
 import numpy as np
 import pytest
 import torch
@@ -13,67 +23,91 @@ pytestmark = pytest.mark.gpu
 
 from oracle import kvlinc_oracle as orc  # noqa: E402
 from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache  # noqa: E402
-from kvlc_testutil import bf16_round  # noqa: E402
 
 D = 128
+S_TOL, OUT_TOL = 1e-5, 1e-3  # T3, T4
 
 
 def _bf16(shape, g):
     return torch.from_numpy(g.standard_normal(shape).astype(np.float32)).bfloat16()
 
 
-def _check_units(cache, k, v, q, units, bank_seeds, chunk_sample, s_tol=1e-5, out_tol=1e-3):
+def _oracle_unit(args):
+    kk, vv, seed = args
+    ad = orc.init_adapter(D, 256, seed=seed)
+    return orc.build_cache(kk, vv, ad)
+
+
+def _oracle_caches(k, v, units, seeds):
+    jobs = [(k[b, h].float().numpy().astype(np.float64), v[b, h].float().numpy().astype(np.float64), seeds[h])
+            for (b, h) in units]
+    with mp.get_context("fork").Pool(min(len(jobs), max(1, mp.cpu_count()))) as pool:
+        return pool.map(_oracle_unit, jobs)
+
+
+def _check_units(cache, k, v, q, units, seeds):
     Hkv, Hq = cache.Hkv, cache.Hq
     NG = Hq // Hkv
-    out = cache.decode(q.cuda(), adapters=AdapterBank.initialize(Hkv, seeds=bank_seeds), out_dtype=torch.float32)
+    out = cache.decode(q.cuda(), adapters=AdapterBank.initialize(Hkv, seeds=seeds), out_dtype=torch.float32)
     out = out.cpu().numpy()
     qn = q.float().numpy().astype(np.float64)
-    for (b, h) in units:
-        ad = orc.init_adapter(D, 256, seed=bank_seeds[h])
-        kk = k[b, h].float().numpy().astype(np.float64)
-        vv = v[b, h].float().numpy().astype(np.float64)
-        oc = orc.build_cache(kk, vv, ad)
-        assert cache.n_chunks[b] == len(oc.key_chunks)
-        for ci in chunk_sample(len(oc.key_chunks)):
-            ex = cache.export_chunk(b, h, ci)
+    worst = {"S": 0.0, "P": 0.0, "out": 0.0}
+    for (b, h), oc in zip(units, _oracle_caches(k, v, units, seeds)):
+        n = len(oc.key_chunks)
+        assert int(cache.n_chunks[b]) == n
+        ex = cache.export_unit(b, h, n)
+        for ci in range(n):  # T1 / T2 on every chunk
             ch = oc.key_chunks[ci]
-            assert np.array_equal(ex["kwords"], ch.words), (b, h, ci)
-            assert np.array_equal(ex["kscale"], ch.scales[0].astype(np.float16)), (b, h, ci)
             sl = slice(ci * 128, (ci + 1) * 128)
-            assert np.array_equal(ex["vwords"], oc.value_words[sl]), (b, h, ci)
-            assert np.array_equal(ex["vzero"], oc.value_zeros[sl, 0].astype(np.float16)), (b, h, ci)
+            assert np.array_equal(ex["kwords"][ci], ch.words), (b, h, ci)
+            assert np.array_equal(ex["kscale"][ci], ch.scales[0].astype(np.float16)), (b, h, ci)
+            assert np.array_equal(ex["kzero"][ci], ch.zeros[0].astype(np.float16)), (b, h, ci)
+            assert np.array_equal(ex["vwords"][ci], oc.value_words[sl]), (b, h, ci)
+            assert np.array_equal(ex["vscale"][ci], oc.value_scales[sl, 0].astype(np.float16)), (b, h, ci)
+            assert np.array_equal(ex["vzero"][ci], oc.value_zeros[sl, 0].astype(np.float16)), (b, h, ci)
         u = b * Hkv + h
         S = cache.S[u].double().cpu().numpy()
-        assert np.linalg.norm(S - oc.s_state) <= s_tol * np.linalg.norm(oc.s_state), (b, h)
+        P = cache.P[u].double().cpu().numpy()
+        es = np.linalg.norm(S - oc.s_state) / np.linalg.norm(oc.s_state)
+        ep = np.linalg.norm(P - oc.p_state) / np.linalg.norm(oc.p_state)
+        assert es <= S_TOL and ep <= S_TOL, (b, h, es, ep)
+        ad = orc.init_adapter(D, 256, seed=seeds[h])
         ocm = orc.fp16_meta_copy(oc)
         for i in range(NG):
             ref = orc.decode_blocked(qn[b, h * NG + i], ocm, ad)
-            err = np.abs(out[b, h * NG + i] - ref).max()
-            assert err <= out_tol * np.abs(ref).max(), (b, h, i, err)
+            err = np.abs(out[b, h * NG + i] - ref).max() / np.abs(ref).max()
+            assert err <= OUT_TOL, (b, h, i, err)
+            worst["out"] = max(worst["out"], err)
+        worst["S"], worst["P"] = max(worst["S"], es), max(worst["P"], ep)
+    print("worst", {k2: f"{v2:.2e}" for k2, v2 in worst.items()})
 
 
-@pytest.mark.parametrize("cfg", ["config2", "config3"])
-def test_full_batch_8k_sampled_units(cfg):
-    B, Hkv, Hq, n = (16, 8, 32, 8192) if cfg == "config2" else (16, 4, 28, 8192)
-    g = orc.rng(2024 if cfg == "config2" else 2025)
-    k, v, q = _bf16((B, Hkv, n, D), g), _bf16((B, Hkv, n, D), g), _bf16((B, Hq, D), g)
-    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
-    seeds = list(range(Hkv))
-    cache.prefill(k.cuda(), v.cuda(), adapters=AdapterBank.initialize(Hkv, seeds=seeds))
-    units = [(0, 0), (7, Hkv - 1), (15, Hkv // 2)]
-    _check_units(cache, k, v, q, units, seeds, lambda nc: [0, nc // 2, nc - 1])
+def _sample_units(B, Hkv, n_units, seed):
+    if B * Hkv <= n_units:
+        return [(b, h) for b in range(B) for h in range(Hkv)]
+    r = np.random.default_rng(seed)
+    picks = r.choice(B * Hkv, size=n_units, replace=False)
+    # always include the first and the last unit
+    picks[0], picks[-1] = 0, B * Hkv - 1
+    return [(int(p) // Hkv, int(p) % Hkv) for p in sorted(set(int(x) for x in picks))]
 
 
-def test_config4_128k_one_sequence_sampled_unit():
-    B, Hkv, Hq, n = 1, 8, 32, 131072
-    g = orc.rng(2026)
+CONFIGS = {
+    "config2_b16_8k": (16, 8, 32, 8192, 2024),
+    "config3_b1_4k": (1, 4, 28, 4096, 2027),
+    "config3_b16_8k": (16, 4, 28, 8192, 2025),
+    "config3_b64_32k": (64, 4, 28, 32768, 2028),
+    "config4_b1_128k": (1, 8, 32, 131072, 2026),
+}
+
+
+@pytest.mark.parametrize("cfg", list(CONFIGS))
+def test_full_size_sampled_units_every_chunk(cfg):
+    B, Hkv, Hq, n, seed = CONFIGS[cfg]
+    g = orc.rng(seed)
     k, v, q = _bf16((B, Hkv, n, D), g), _bf16((B, Hkv, n, D), g), _bf16((B, Hq, D), g)
     cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
     seeds = list(range(Hkv))
     cache.prefill(k.cuda(), v.cuda(), adapters=AdapterBank.initialize(Hkv, seeds=seeds))
     assert int(cache.n_chunks[0]) == (n - 128) // 128
-    # T3 / T4 stated for a 131k-token state: the fp32 tensor-core accumulation
-    # of S measures 1.9e-5 relative (4.5e-6 at 8k, growing ~ sqrt(n)); the decode output, an
-    # average over 131k values (max|out| ~ 0.016) against O(1) correction terms, carries that
-    # state error as 1.4e-3 .. 2.0e-3 of max|out| (north_star's stated example: 1e-2)
-    _check_units(cache, k, v, q, [(0, 3)], seeds, lambda nc: [0, 511, nc - 1], s_tol=3e-5, out_tol=3e-3)
+    _check_units(cache, k, v, q, _sample_units(B, Hkv, 8, seed), seeds)
