@@ -78,6 +78,10 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // mean) and the zero term accumulates the row midpoint z' = z + 3/2 s instead of z:
 // both sums stay small and the truncation acts on small values.
 // ps: this lane's sum of p s of the chunk per column group e (heads t / 2t + e).
+#ifndef KVLC_CENTRE
+#define KVLC_CENTRE 1
+#endif
+constexpr bool CENTRE = KVLC_CENTRE;
 template <int NG>
 __device__ __forceinline__ void centre_acc(WarpState<NG>& st, float (&ps)[WarpState<NG>::NH]) {
   constexpr bool HILO = NG <= 4;
@@ -320,7 +324,7 @@ __device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSm
   for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const float sv = svs[2 * mt + r], zv = fmaf(1.5f, svs[2 * mt + r], svz[2 * mt + r]);  // z' (centre_acc)
+      const float sv = svs[2 * mt + r], zv = CENTRE ? fmaf(1.5f, svs[2 * mt + r], svz[2 * mt + r]) : svz[2 * mt + r];  // z' (centre_acc)
       if (HILO) {
         const float p = fast_exp2(cq[mt][2 * r] - st.m[0]);
         st.l[0] += p;
@@ -376,7 +380,7 @@ __device__ __forceinline__ void quant_chunk(const ChunkStage& stg, const QuantSm
       }
     }
   }
-  centre_acc<NG>(st, ps);
+  if (CENTRE) centre_acc<NG>(st, ps);
 }
 
 // Writes this warp's record (m_ref, l, m_true, -, y[c]) per head into shared memory.

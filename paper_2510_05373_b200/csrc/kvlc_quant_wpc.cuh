@@ -220,7 +220,7 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
     for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        const float sv = svs[2 * mt + r], zv = fmaf(1.5f, svs[2 * mt + r], svz[2 * mt + r]);  // z' (centre_acc)
+        const float sv = svs[2 * mt + r], zv = CENTRE ? fmaf(1.5f, svs[2 * mt + r], svz[2 * mt + r]) : svz[2 * mt + r];  // z' (centre_acc)
         if (HILO) {
           const float p = fast_exp2(cq[s][mt][2 * r] - st.m[0]);
           st.l[0] += p;
@@ -275,7 +275,7 @@ __device__ __forceinline__ void wpc_chunk(const HalfStage& kst, const HalfStage&
       }
     }
   }
-  centre_acc<NG>(st, ps);
+  if (CENTRE) centre_acc<NG>(st, ps);
 }
 
 // A quantized split, warp per chunk: chunks [lo, hi) of one unit, warp w takes lo + w + 4i.
