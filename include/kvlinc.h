@@ -81,9 +81,12 @@ int kvlc_ref_dequantize(const uint32_t* words, const double* scales,
                         const double* zeros, int64_t rows, int64_t cols,
                         int bits, int group, int axis, double* out, void* stream);
 
-/* rotate (hadamard.py:45-57) as a fast Walsh-Hadamard transform in float64:
- * post: out = x @ H (x [rows][dim]);  pre: out = H @ x (x [dim][cols]).
- * dim must be a power of two <= 4096. */
+/* rotate (hadamard.py:45-57) in float64 as the reference computes it: a dense
+ * product with the Sylvester matrix H (sequential FMA over the inner index, the
+ * reference's x @ H order; bit-identical to numpy/OpenBLAS on the golden
+ * vectors).  post: out = x @ H (x [rows][dim]);  pre: out = H @ x (x [dim][cols]).
+ * dim must be a power of two <= 4096.  (The serving flush uses a warp-shuffle
+ * FWHT with an exact fallback near rounding ties.) */
 int kvlc_ref_rotate(const double* x, int64_t rows, int64_t cols, int placement,
                     double* out, void* stream);
 
@@ -149,13 +152,20 @@ int kvlc_ref_decode(const double* q, int d, int group, int bits, int rotated,
 
 /* Device cache descriptor (POD; every pointer is device memory).
  * One (b, kv-head) pair is a "unit".  Layouts (u = b*Hkv + kvh):
- *   kcodes [u][max_chunks][8][128] u32  word (w, c) = tokens 16w..16w+15 of
- *          channel c — byte-identical to the reference's channel-axis chunk
- *          codes (quantize.py:157-160, cache.py:141).
- *   vcodes [u][max_chunks][8][128] u32  word (j, p) = channels 16j..16j+15 of
- *          the token in slot p; slot p = 16*((t%32)/4) + 4*(t/32) + t%4 for
- *          chunk token t (a transpose + permutation of the reference's
- *          value_rows words; kvlc_export_chunk() restores the reference order).
+ *   kcodes [u][max_chunks][1024] u32, vcodes [u][max_chunks][1024] u32: the
+ *          2-bit codes of a chunk (G = 128 tokens x 128 channels) in the
+ *          decode kernels' fragment-native word order (NOT the reference's
+ *          word order; kvlc_export_chunk() / kvlc_serialize_unit() return the
+ *          reference layout, kvlc_deserialize_unit() writes this one).  Word
+ *          wi = (w*32 + lane)*8 + i, lane = 4*g + t0 (w, g, i in 0..3 / 0..7 /
+ *          0..7, t0 in 0..3) holds 16 codes, code (byte q, pair j) at bit
+ *          (8*q + 2*j + 2) mod 32 (the unrotated word rotated left by 2):
+ *            K word: byte q = channel 16*i + 2*t0 + {0,8,1,9}[q],
+ *                    pair j = token 32*w + 4*g + j;
+ *            V word: byte q = token 32*w + 8*t0 + 2*(i>>2) + {0,1,4,5}[q],
+ *                    pair j = channel 32*(i&3) + 8*j + g.
+ *          (tests/test_gpu_batched.py::test_documented_code_word_layout checks
+ *          this formula against kvlc_export_chunk.)
  *   kscale/kzero [u][max_chunks][128] f16 (per channel), vscale/vzero
  *          [u][max_chunks][128] f16 (per token, natural order).
  *   kres [u][256][128] bf16 (ring slot-major), vres [u][128][256] bf16
@@ -232,15 +242,21 @@ typedef struct kvlc_decode_opts {
  * records per unit (explicit small chunks_per_split) fuse the combine into the
  * last CTA of each (b, kv-head) unit instead.  The launch may overlap the
  * previous kernel on `stream` (programmatic dependent launch): q may be
- * produced by any kernel; cache state must be written through this library
- * (prefill / append / flush_due / deserialize_unit mark the stream so that the
- * next decode on it waits fully).  The workspace must be
+ * produced by any kernel; its first code copies are issued before the
+ * predecessor completes, so cache state must be written through this library
+ * (prefill / a flushing append / flush_due / deserialize_unit mark the CACHE,
+ * independent of host thread and stream, and the next decode of that cache
+ * waits fully) or the writer must call kvlc_note_cache_write().  The workspace must be
  * zero-filled before its first use (its head holds per-unit arrival counters
  * that every launch leaves at zero). */
 size_t kvlc_decode_workspace(const kvlc_cache* cache, const kvlc_decode_opts* o);
 int kvlc_decode(const kvlc_cache* cache, const kvlc_adapter* ad,
                 const uint16_t* q, void* out, const kvlc_decode_opts* o,
                 void* ws, size_t ws_bytes, void* stream);
+
+/* Marks `cache` as written outside this library (codes, metadata or chunk counts):
+ * its next decode launches without overlapping the preceding kernel. */
+void kvlc_note_cache_write(const kvlc_cache* cache);
 
 /* Split-KV across devices.  kvlc_decode_partial computes, for the chunk range
  * [chunk_lo, chunk_hi) of every sequence, one merged record per (b, q-head):

@@ -354,3 +354,75 @@ def test_ring_flush_tensor_core_and_simt_paths_agree():
         check_states(cache, ocs)
     assert torch.equal(caches[0].kcodes, caches[1].kcodes) and torch.equal(caches[0].vcodes, caches[1].vcodes)
     assert torch.equal(caches[0].vscale, caches[1].vscale) and torch.equal(caches[0].kzero, caches[1].kzero)
+
+
+def _rotr2(w):
+    w = w.astype(np.uint64)
+    return (((w >> 2) | (w << 30)) & 0xFFFFFFFF).astype(np.uint32)
+
+
+def test_documented_code_word_layout():
+    """include/kvlinc.h documents the fragment-native kcodes / vcodes word layout; decode the
+    raw device words with that formula and compare with kvlc_export_chunk (reference layout)."""
+    B, Hkv, Hq, n = 1, 2, 8, 640
+    k, v, _ = make_inputs(B, Hkv, Hq, n, seed=31)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 128)
+    cache.prefill(tdev(k), tdev(v), adapters=AdapterBank.initialize(Hkv))
+    nc = int(cache.n_chunks[0])
+    assert nc >= 2
+    koff, voff = [0, 8, 1, 9], [0, 1, 4, 5]
+    for u in range(Hkv):
+        for ci in range(nc):
+            kw = _rotr2(cache.kcodes[u, ci].cpu().numpy().view(np.uint32).reshape(-1))
+            vw = _rotr2(cache.vcodes[u, ci].cpu().numpy().view(np.uint32).reshape(-1))
+            kc = np.zeros((128, 128), np.uint8)  # [token][channel]
+            vc = np.zeros((128, 128), np.uint8)
+            for wi in range(1024):
+                w, lane, i = wi >> 8, (wi >> 3) & 31, wi & 7
+                g, t0 = lane >> 2, lane & 3
+                for q in range(4):
+                    for j in range(4):
+                        code_k = (kw[wi] >> (8 * q + 2 * j)) & 3
+                        code_v = (vw[wi] >> (8 * q + 2 * j)) & 3
+                        kc[32 * w + 4 * g + j, 16 * i + 2 * t0 + koff[q]] = code_k
+                        vc[32 * w + 8 * t0 + 2 * (i >> 2) + voff[q], 32 * (i & 3) + 8 * j + g] = code_v
+            ex = cache.export_chunk(0, u, ci)
+            # reference layouts: key words (8, 128) tokens 16w.. of channel c; value rows (128, 8)
+            want_k = np.zeros((8, 128), np.uint32)
+            want_v = np.zeros((128, 8), np.uint32)
+            for w in range(8):
+                for l in range(16):
+                    want_k[w] |= kc[16 * w + l].astype(np.uint32) << (2 * l)
+            for jw in range(8):
+                for l in range(16):
+                    want_v[:, jw] |= vc[:, 16 * jw + l].astype(np.uint32) << (2 * l)
+            assert np.array_equal(ex["kwords"], want_k), (u, ci)
+            assert np.array_equal(ex["vwords"], want_v), (u, ci)
+
+
+def test_decode_right_after_prefill_from_another_thread():
+    """prefill writes codes and chunk counts that the decode reads before its
+    griddepcontrol.wait.  The write mark lives with the cache (not the host thread or the
+    stream), so a decode issued by another thread right after a prefill, with no host
+    sync, still waits for it.  Two caches back to back in the same stream: prefill A,
+    prefill B, decode A, decode B (each decode follows a writer of a different cache)."""
+    import threading
+    B, Hkv, Hq, n = 2, 2, 8, 700
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=41)
+    oads = [orc.init_adapter(D, 256, seed=h) for h in range(Hkv)]
+    bank = AdapterBank.initialize(Hkv)
+    caches = [BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256) for _ in range(2)]
+    kd, vd, qd = tdev(k), tdev(v), tdev(q)
+    torch.cuda.synchronize()
+
+    def writer():
+        for c in caches:
+            c.prefill(kd, vd, adapters=bank)
+
+    th = threading.Thread(target=writer)
+    th.start()
+    th.join()  # host order only: the GPU work is still queued, nothing synchronised
+    outs = [c.decode(qd, adapters=bank, out_dtype=F32) for c in caches]
+    ref = oracle_decode(q, oracle_caches(k, v, [n] * B, oads), oads)
+    for out in outs:
+        assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3 * np.abs(ref).max()
