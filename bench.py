@@ -100,6 +100,31 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+# ----------------------------------------------------------------------------- traffic
+DECODE_SOURCES = ("kvlc_decode.cu", "kvlc_quant.cuh", "kvlc_quant_wpc.cuh", "kvlc_common.cuh", "kvlc_tc.cuh")
+
+
+def decode_source_hash():
+    import hashlib
+    h = hashlib.sha256()
+    for f in DECODE_SOURCES:
+        h.update(open(os.path.join(ROOT, "paper_2510_05373_b200", "csrc", f), "rb").read())
+    return h.hexdigest()
+
+
+def traffic_record():
+    """dram__bytes_read + write per split_kernel launch from the committed ncu capture
+    (profiles/split_kernel_traffic.json, tools/update_traffic.py), used only while the hash
+    of the decode sources it was captured from matches the sources being benchmarked."""
+    tpath = os.path.join(ROOT, "profiles", "split_kernel_traffic.json")
+    if not os.path.exists(tpath):
+        return None, "no capture"
+    t = json.load(open(tpath))
+    if t.get("source_sha256") != decode_source_hash():
+        return None, "stale: the decode sources changed since the ncu capture"
+    return t.get("dram_bytes_per_launch"), f"ncu --set full capture {t.get('capture', '')}".strip()
+
+
 # ----------------------------------------------------------------------------- ours
 def run_ours(args, rank, world, local_rank):
     import torch
@@ -189,23 +214,25 @@ def run_ours(args, rank, world, local_rank):
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / K
+    del graphs_e2e
 
     times = torch.tensor([step_ms, split_ms, e2e_ms], device=dev)
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
     step_ms, split_ms, e2e_ms = (float(x) for x in times.tolist())
-    if rank != 0:
-        return None
-
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak_gbs = float(peaks.get("hbm_gbs", 6650.0))
+    multi = None
+    if world > 1 and not args.no_extra:   # every rank takes part (collectives)
+        torch.cuda.empty_cache()
+        multi = run_multi_gpu(args, rank, world, dev, peak_gbs)
+    if rank != 0:
+        return None
+
     step_bytes = algo_bytes_step(B, HKV, HQ, nq, nr)
     achieved = step_bytes / (split_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "split_kernel_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+    traffic, traffic_note = traffic_record()
 
     result = {
         "metric": METRIC, "value": B * world / (step_ms * 1e-3), "unit": "tokens/s",
@@ -217,7 +244,7 @@ def run_ours(args, rank, world, local_rank):
         "us_per_step": step_ms * 1e3,
         "hbm_gbs_step": step_bytes / (step_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_gbs, "unit": "GB/s",
-                     "frac": achieved / peak_gbs, "traffic": traffic,
+                     "frac": achieved / peak_gbs, "traffic": traffic, "traffic_source": traffic_note,
                      "kernel": "split_kernel + combine_kernel (kvlc_decode.cu, the PDL-chained pair "
                                "of one step; traffic: split_kernel)", "split_us": split_ms * 1e3,
                      "algorithmic_bytes_per_launch": step_bytes,
@@ -237,11 +264,18 @@ def run_ours(args, rank, world, local_rank):
                   "(LSE merge per (b, q-head)), chained by programmatic dependent launch",
         "clocks": clk.summary(),
     }
+    if multi is not None:
+        result["multi_gpu"] = multi
     if world == 1 and not args.no_fa:
         result["bf16_flash_attn"] = run_flash_attn(args, dev, step_ms)
+        result["bf16_flashinfer"] = run_flashinfer(args, dev, step_ms)
+        fa_us = [x["us_per_step"] for x in (result["bf16_flash_attn"], result["bf16_flashinfer"])
+                 if "us_per_step" in x]
+        if fa_us:
+            result["speedup_vs_best_bf16"] = min(fa_us) / (step_ms * 1e3)
     if world == 1 and not args.no_extra:
         result["serving_loop"] = run_serving_loop(caches[0], q, bank, dev)
-        del caches, graphs_e2e
+        del caches
         torch.cuda.empty_cache()
         result["other_configs"] = run_other_configs(dev, peak_gbs)
     if world == 1 and not args.no_cpu:
@@ -249,22 +283,53 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
-def _time_decode(cache, q, bank, steps=20, warmup=5):
+def _time_rotating(caches, q, bank, reps=6):
+    """Mean decode-step time over a CUDA graph of back-to-back launches that rotate over
+    `caches` (replicas whose bytes together exceed the L2, so every launch streams from HBM)."""
     import torch
     out = torch.empty_like(q)
-    for _ in range(warmup):
-        cache.decode(q, adapters=bank, out=out)
-    g = cache.capture_decode(q, adapters=bank, out=out)[0]
-    for _ in range(warmup):
-        g.replay()
+    for c in caches:
+        c.decode(q, adapters=bank, out=out)
+    kg = 4 * len(caches) if len(caches) > 1 else 8
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(kg):
+            caches[i % len(caches)].decode(q, adapters=bank, out=out)
+    g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(steps):
+    for _ in range(reps):
         g.replay()
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / steps
+    return e0.elapsed_time(e1) / (reps * kg)
+
+
+def _decode_point(dev, b, hkv, hq, n, peak_gbs):
+    """One decode shape, timed over L2-cold rotating replicas (>= 300 MB streamed per cycle)."""
+    import torch
+    from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache, flush_count
+    nq = int(flush_count([n])[0]) * G
+    nbytes = algo_bytes_step(b, hkv, hq, nq, n - nq)
+    nrep = max(1, min(6, -(-300_000_000 // nbytes)))
+    bank = AdapterBank.initialize(hkv, device=dev)
+    caches = []
+    for _ in range(nrep):
+        c = BatchedKVCache(b, hkv, hq, n + 256, device=dev)
+        k = torch.randn(b, hkv, n, D, device=dev).bfloat16()
+        v = torch.randn(b, hkv, n, D, device=dev).bfloat16()
+        c.prefill(k, v, adapters=bank)
+        del k, v
+        caches.append(c)
+    q = torch.randn(b, hq, D, device=dev).bfloat16()
+    ms = _time_rotating(caches, q, bank)
+    del caches
+    torch.cuda.empty_cache()
+    return {"us_per_step": ms * 1e3, "tokens_per_s": b / (ms * 1e-3), "hbm_gbs": nbytes / (ms * 1e-3) / 1e9,
+            "roofline_frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs, "algorithmic_bytes": nbytes,
+            "l2": f"{nrep} rotating replicas ({nrep * nbytes / 1e6:.0f} MB per cycle)" if nrep > 1
+                  else "single cache larger than L2"}
 
 
 def run_serving_loop(cache, q, bank, dev):
@@ -304,30 +369,18 @@ def run_serving_loop(cache, q, bank, dev):
 
 
 def run_other_configs(dev, peak_gbs):
-    """BASELINE configs 3-5 on this GPU (one point each; single cache, so config 4's
-    78 MB can be partly L2-resident -- stated).  Configs 3 / 4 time the same fused
-    decode step (CUDA graph); config 5 times kvlc_prefill (quantize/pack + FWHT +
-    adapter-state update) of Qwen3-8B shapes."""
+    """BASELINE configs 3-5 on this GPU.  Configs 3 / 4 time the same fused decode step
+    over L2-cold rotating replicas; config 3 also as the batch x context sweep of
+    BASELINE.json (B 1 / 16 / 64 x ctx 4k / 32k, plus the B16 x 8k point); config 5 times
+    kvlc_prefill (quantize/pack + FWHT + adapter-state update) of Qwen3-8B shapes."""
     import torch
     from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache, flush_count
-    out = {}
-    for name, (b, hkv, hq, n) in {"config3_qwen2.5-7b_b16_ctx8k": (16, 4, 28, 8192),
-                                  "config4_llama3-8b_b1_ctx128k": (1, 8, 32, 131072)}.items():
-        bank = AdapterBank.initialize(hkv, device=dev)
-        c = BatchedKVCache(b, hkv, hq, n + 256, device=dev)
-        k = torch.randn(b, hkv, n, D, device=dev).bfloat16()
-        v = torch.randn(b, hkv, n, D, device=dev).bfloat16()
-        c.prefill(k, v, adapters=bank)
-        del k, v
-        q = torch.randn(b, hq, D, device=dev).bfloat16()
-        ms = _time_decode(c, q, bank)
-        nq = int(flush_count([n])[0]) * G
-        nbytes = algo_bytes_step(b, hkv, hq, nq, n - nq)
-        out[name] = {"us_per_step": ms * 1e3, "tokens_per_s": b / (ms * 1e-3),
-                     "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "roofline_frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs,
-                     "algorithmic_bytes": nbytes}
-        del c
-        torch.cuda.empty_cache()
+    out = {"config3_qwen2.5-7b_b16_ctx8k": _decode_point(dev, 16, 4, 28, 8192, peak_gbs),
+           "config4_llama3-8b_b1_ctx128k": _decode_point(dev, 1, 8, 32, 131072, peak_gbs)}
+    sweep = {}
+    for b, n in ((1, 4096), (16, 4096), (64, 4096), (1, 32768), (16, 32768), (64, 32768)):
+        sweep[f"b{b}_ctx{n // 1024}k"] = _decode_point(dev, b, 4, 28, n, peak_gbs)
+    out["config3_sweep_qwen2.5-7b"] = sweep
     # config 5: prefill of 32k tokens x 8 kv heads (Qwen3-8B attention shapes)
     b, hkv, n = 1, 8, 32768
     bank = AdapterBank.initialize(hkv, device=dev)
@@ -353,6 +406,98 @@ def run_other_configs(dev, peak_gbs):
         "us_per_step": ms * 1e3, "kv_head_tokens_per_s": b * hkv * n / (ms * 1e-3),
         "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "roofline_frac": nbytes / (ms * 1e-3) / 1e9 / peak_gbs,
         "kernel": "quant_kernel (codes, FWHT, operand images) + flush_tc_kernel (tcgen05: 3-pass fp16 phi_k GEMM, 2-pass S GEMM on exact codes, TMEM accumulators)"}
+    return out
+
+
+def run_multi_gpu(args, rank, world, dev, peak_gbs):
+    """N > 1 only: the partitioned configs of BASELINE.json on the whole job.
+      * strong scaling, configs 2 and 3: a fixed global batch of 16 sequences sharded by
+        batch across the ranks ((b, kv-head) units are independent: no collective);
+      * config 4 split-KV: one 131k-token sequence, chunks split contiguously across the
+        ranks (distributed.plan_sequence_shards), S / P all-reduced once after prefill,
+        each step = kvlc_decode_partial on every rank + ONE all-gather of [record |
+        correction] over NCCL + kvlc_merge_records (SequenceShardedDecoder).
+    Every time is the max over ranks of CUDA-event time on each rank's stream."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache, merge_records
+    from paper_2510_05373_b200.distributed import (GpuOps, SequenceShardedDecoder, allreduce_states,
+                                                   plan_sequence_shards)
+
+    def tmax(x):
+        t = torch.tensor([float(x)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    out = {}
+    for name, (hkv, hq, n) in {"config2_strong_b16_ctx8k": (8, 32, 8192),
+                               "config3_strong_b16_ctx8k": (4, 28, 8192)}.items():
+        if 16 % world:
+            out[name] = {"skipped": f"global batch 16 does not shard evenly over {world} GPUs"}
+            continue
+        bl = 16 // world
+        dist.barrier()
+        pt = _decode_point(dev, bl, hkv, hq, n, peak_gbs)
+        us = tmax(pt["us_per_step"])
+        out[name] = {"scaling": "strong", "global_batch": 16, "batch_per_gpu": bl, "us_per_step": us,
+                     "tokens_per_s": 16 / (us * 1e-6), "algorithmic_bytes_per_gpu": pt["algorithmic_bytes"],
+                     "roofline_frac_per_gpu": pt["algorithmic_bytes"] / (us * 1e-6) / 1e9 / peak_gbs,
+                     "comm": "none (units independent)"}
+    # config 4: sequence-parallel split-KV
+    n, hkv, hq = 131072, 8, 32
+    shards = plan_sequence_shards(n, world)
+    sh = shards[rank]
+    gen = torch.Generator(device=dev).manual_seed(4242)   # every rank draws the same sequence
+    k = torch.randn(1, hkv, n, D, device=dev, generator=gen).bfloat16()
+    v = torch.randn(1, hkv, n, D, device=dev, generator=gen).bfloat16()
+    q = torch.randn(1, hq, D, device=dev, generator=gen).bfloat16()
+    bank = AdapterBank.initialize(hkv, device=dev)
+    cache = BatchedKVCache(1, hkv, hq, sh.tok_hi - sh.tok_lo + 256, device=dev)
+    cache.prefill(k[:, :, sh.tok_lo:sh.tok_hi].contiguous(), v[:, :, sh.tok_lo:sh.tok_hi].contiguous(),
+                  adapters=bank, keep_window=sh.tail)
+    del k, v
+    allreduce_states(cache)
+    ops = GpuOps(cache, bank)
+    dec = SequenceShardedDecoder(sh, ops)
+    K, W = args.steps, args.warmup
+    for _ in range(W):
+        dec.decode(q)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        o = dec.decode(q)
+    e1.record()
+    torch.cuda.synchronize()
+    step_us = tmax(e0.elapsed_time(e1) * 1e3 / K)
+    dist.barrier()
+    e0.record()
+    for _ in range(K):
+        rec, corr = ops.partial(q, sh.tail)
+    e1.record()
+    torch.cuda.synchronize()
+    part_us = tmax(e0.elapsed_time(e1) * 1e3 / K)
+    send = torch.cat([rec, corr], dim=-1).contiguous()
+    buf = torch.empty((world * send.shape[0],) + tuple(send.shape[1:]), dtype=send.dtype, device=dev)
+    dist.barrier()
+    e0.record()
+    for _ in range(K):
+        dist.all_gather_into_tensor(buf, send)
+        b4 = buf.view((world,) + tuple(send.shape))
+        merge_records(b4[..., :rec.shape[-1]].contiguous(), b4[world - 1, ..., rec.shape[-1]:].contiguous())
+    e1.record()
+    torch.cuda.synchronize()
+    merge_us = tmax(e0.elapsed_time(e1) * 1e3 / K)
+    nq_local = int(cache.n_chunks[0]) * G
+    local_bytes = algo_bytes_step(1, hkv, hq, nq_local, int(cache.res_len[0]) if sh.tail else 0)
+    out["config4_splitkv_b1_ctx128k"] = {
+        "scaling": "strong", "comm_nranks": world, "us_per_step": step_us, "tokens_per_s": 1 / (step_us * 1e-6),
+        "partial_us": part_us, "allgather_merge_us": merge_us,
+        "chunks_per_rank": [s2.chunk_hi - s2.chunk_lo for s2 in shards],
+        "algorithmic_bytes_per_gpu_rank": local_bytes,
+        "collective": "one NCCL all_gather per step of [record | correction] (B x Hq x 389 fp32 per rank)",
+        "out_finite": bool(torch.isfinite(o).all().item())}
     return out
 
 
@@ -382,11 +527,45 @@ def run_flash_attn(args, dev, ours_ms):
             "hbm_gbs": fa_bytes / (fa_ms * 1e-3) / 1e9, "speedup_ours_vs_fa": fa_ms / ours_ms}
 
 
+def run_flashinfer(args, dev, ours_ms):
+    """bf16 FlashInfer batch decode (paged KV, 16-token pages) on the same shapes."""
+    import torch
+    try:
+        import flashinfer
+        page = 16
+        npages = CTX // page
+        kv = torch.randn(B * npages, 2, page, HKV, D, device=dev).bfloat16()
+        q = torch.randn(B, HQ, D, device=dev).bfloat16()
+        indptr = torch.arange(0, B + 1, device=dev, dtype=torch.int32) * npages
+        indices = torch.arange(0, B * npages, device=dev, dtype=torch.int32)
+        last = torch.full((B,), page, dtype=torch.int32, device=dev)
+        wsbuf = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+        w = flashinfer.BatchDecodeWithPagedKVCacheWrapper(wsbuf, "NHD")
+        w.plan(indptr, indices, last, HQ, HKV, D, page, q_data_type=torch.bfloat16, kv_data_type=torch.bfloat16)
+        for _ in range(args.warmup):
+            w.run(q, kv)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            w.run(q, kv)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+    except Exception as e:  # pragma: no cover
+        return {"unavailable": f"{type(e).__name__}: {e}"[:300]}
+    fb = 2 * B * CTX * HKV * D * 2 + 2 * B * HQ * D * 2
+    return {"impl": f"flashinfer {getattr(flashinfer, '__version__', '?')} BatchDecodeWithPagedKVCacheWrapper "
+                    f"(bf16 KV, page {page})", "us_per_step": ms * 1e3, "hbm_gbs": fb / (ms * 1e-3) / 1e9,
+            "speedup_ours_vs_flashinfer": ms / ours_ms}
+
+
 # ----------------------------------------------------------------------------- CPU reference
 def _oracle_unit_worker(args):
     """One (b, kv-head) unit of the workload on one core: build its cache with the
     oracle's streaming rule, then time decode_step_blocked for its g q-heads."""
-    kvh, reps, seed = args
+    kvh, reps, seed = args[:3]
+    as_is = len(args) > 3 and args[3]
     from threadpoolctl import threadpool_limits
     import numpy as np
     from oracle import kvlinc_oracle as orc
@@ -401,21 +580,27 @@ def _oracle_unit_worker(args):
         for _ in range(reps):
             t = time.perf_counter()
             for h in range(HQ // HKV):
-                orc.decode_blocked(qs[h], cache, ad)
+                orc.decode_blocked(qs[h], cache, ad, as_is=as_is)
             times.append(time.perf_counter() - t)
         return times
 
 
 def cpu_baseline_sample():
     """Single-core sample: one kv unit (4 q-heads) of the workload, extrapolated
-    to the full step (B*Hkv = 128 units)."""
+    to the full step (B*Hkv = 128 units); the O(N) value-slicing port (median of 3) and,
+    once, the reference's as-is order (whole value store dequantized per block,
+    cache.py:110, O(N^2 / G); identical outputs)."""
     t_unit = statistics.median(_oracle_unit_worker((0, 3, 7)))
+    t_asis = _oracle_unit_worker((0, 1, 7, True))[0]
     step_s = t_unit * B * HKV
     return {"value": B / step_s, "unit": "tokens/s", "cores": 1, "kind": "port",
             "sample": f"1 of {B * HKV} (b, kv-head) units, {HQ // HKV} q-heads, ctx {CTX}, "
                       f"oracle decode_step_blocked (O(N) value slicing), median of 3; "
                       f"{t_unit * 1e3:.1f} ms per unit, extrapolated x{B * HKV}",
-            "ms_per_step": step_s * 1e3}
+            "ms_per_step": step_s * 1e3,
+            "as_is": {"value": B / (t_asis * B * HKV), "unit": "tokens/s", "ms_per_unit": t_asis * 1e3,
+                      "sample": "same unit, the reference's whole-store value dequantization per block "
+                                "(cache.py:110), 1 run"}}
 
 
 def run_reference(args, world):
@@ -462,8 +647,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # KVLC_BENCH_BACKEND=gloo with more ranks than GPUs: a functional check of the
+        # multi-rank code paths on one GPU (ranks share it; numbers are not timings of N GPUs)
+        backend = os.environ.get("KVLC_BENCH_BACKEND", "nccl")
+        local_rank = local_rank % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     result = run_ours(args, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(result), flush=True)

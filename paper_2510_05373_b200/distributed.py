@@ -82,16 +82,20 @@ class SequenceShardedDecoder:
         self.group = group
 
     def decode(self, q: torch.Tensor, literal: bool = False) -> torch.Tensor:
+        """One collective per step: every rank's record and correction row travel in one
+        all-gather buffer ([rec | corr] per (b, q-head)); the merge takes the tail owner's
+        correction (the other ranks' rows are zero)."""
         world = dist.get_world_size(self.group)
         rec, corr = self.ops.partial(q, self.shard.tail)
-        rec = rec.contiguous()
-        recs = torch.empty((world * rec.shape[0],) + tuple(rec.shape[1:]), dtype=rec.dtype,
-                           device=rec.device)
-        dist.all_gather_into_tensor(recs, rec, group=self.group)
-        recs = recs.view((world,) + tuple(rec.shape))
-        # only the tail owner holds a non-zero correction record
-        dist.all_reduce(corr, op=dist.ReduceOp.SUM, group=self.group)
-        return self.ops.merge(recs, corr, literal)
+        wr = rec.shape[-1]
+        send = torch.cat([rec, corr.to(rec.dtype)], dim=-1).contiguous()
+        buf = torch.empty((world * send.shape[0],) + tuple(send.shape[1:]), dtype=send.dtype,
+                          device=send.device)
+        dist.all_gather_into_tensor(buf, send, group=self.group)
+        buf = buf.view((world,) + tuple(send.shape))
+        recs = buf[..., :wr].contiguous()
+        corr_all = buf[world - 1, ..., wr:].contiguous()
+        return self.ops.merge(recs, corr_all, literal)
 
 
 def allreduce_states(cache, group=None):

@@ -111,3 +111,56 @@ def test_full_size_sampled_units_every_chunk(cfg):
     cache.prefill(k.cuda(), v.cuda(), adapters=AdapterBank.initialize(Hkv, seeds=seeds))
     assert int(cache.n_chunks[0]) == (n - 128) // 128
     _check_units(cache, k, v, q, _sample_units(B, Hkv, 8, seed), seeds)
+
+
+def test_config4_sequence_sharded_split_kv_on_one_gpu():
+    """The split-KV path of distributed.SequenceShardedDecoder at config 4 (one 131k-token
+    sequence), its ranks played by 4 shard caches on this GPU: each shard prefills its token
+    range (keep_window=False except the tail owner), S / P are summed into the tail (the
+    all-reduce), each shard emits one record per (b, q-head) over its own chunks
+    (kvlc_decode_partial), the tail's correction row rides along, and kvlc_merge_records
+    merges them.  Checked against the single-cache decode and, for two kv heads, against
+    the oracle at T4."""
+    from paper_2510_05373_b200.batched import merge_records
+    from paper_2510_05373_b200.distributed import plan_sequence_shards
+    B, Hkv, Hq, n, world = 1, 8, 32, 131072, 4
+    g = orc.rng(2029)
+    k, v, q = _bf16((B, Hkv, n, D), g), _bf16((B, Hkv, n, D), g), _bf16((B, Hq, D), g)
+    seeds = list(range(Hkv))
+    bank = AdapterBank.initialize(Hkv, seeds=seeds)
+    kd, vd, qd = k.cuda(), v.cuda(), q.cuda()
+    full = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    full.prefill(kd, vd, adapters=bank)
+    ref_full = full.decode(qd, adapters=bank, out_dtype=torch.float32)
+    shards = plan_sequence_shards(n, world)
+    caches = []
+    for sh in shards:
+        c = BatchedKVCache(B, Hkv, Hq, max_tokens=sh.tok_hi - sh.tok_lo + 256)
+        c.prefill(kd[:, :, sh.tok_lo:sh.tok_hi].contiguous(), vd[:, :, sh.tok_lo:sh.tok_hi].contiguous(),
+                  adapters=bank, keep_window=sh.tail)
+        assert int(c.n_chunks[0]) == sh.chunk_hi - sh.chunk_lo
+        caches.append(c)
+    tail = caches[-1]
+    for c in caches[:-1]:  # the S / P all-reduce, into the tail owner
+        tail.S += c.S
+        tail.P += c.P
+    recs, corr = [], None
+    for sh, c in zip(shards, caches):
+        rec, cr = c.decode_partial(qd, 0, int(c.n_chunks[0]), sh.tail, adapters=bank)
+        recs.append(rec)
+        if sh.tail:
+            corr = cr
+    merged = merge_records(torch.stack(recs), corr, out_dtype=torch.float32)
+    e = (merged - ref_full).abs().max().item() / ref_full.abs().max().item()
+    assert e <= 2e-4, e
+    out = merged.cpu().numpy()
+    qn = q.float().numpy().astype(np.float64)
+    units = [(0, 0), (0, Hkv - 1)]
+    NG = Hq // Hkv
+    for (b, h), oc in zip(units, _oracle_caches(k, v, units, seeds)):
+        ad = orc.init_adapter(D, 256, seed=seeds[h])
+        ocm = orc.fp16_meta_copy(oc)
+        for i in range(NG):
+            ref = orc.decode_blocked(qn[b, h * NG + i], ocm, ad)
+            err = np.abs(out[b, h * NG + i] - ref).max() / np.abs(ref).max()
+            assert err <= OUT_TOL, (b, h, i, err)
