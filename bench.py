@@ -333,21 +333,23 @@ def _decode_point(dev, b, hkv, hq, n, peak_gbs):
 
 
 def run_serving_loop(cache, q, bank, dev):
-    """Config-2 decode loop with appends: steady-state steps replay one CUDA graph (append one
-    token per sequence + fused decode, BatchedKVCache.capture_serving_step); every 128 steps all
-    sequences flush (lockstep batch), run eagerly.  Mutates `cache`."""
+    """Config-2 decode loop with appends, every step a CUDA graph launch
+    (BatchedKVCache.capture_serving_step): steady steps append one token per sequence +
+    fused decode; every 128 steps all sequences flush in lockstep (the worst case: real
+    batches stagger their flushes), a step whose graph also holds the tensor-core ring
+    flush.  The graphs of a period are captured ahead (step.prepare()).  Mutates `cache`."""
     import torch
     kt = torch.randn(cache.B, cache.Hkv, D, device=dev).bfloat16()
     vt = torch.randn(cache.B, cache.Hkv, D, device=dev).bfloat16()
     step, out = cache.capture_serving_step(q, kt, vt, adapters=bank)
-    # one full flush period first: the process's first flush pays one-time setup (~1.3 ms)
-    for _ in range(cache.steps_until_flush()):
+    # one full flush period first (the process's first flush pays one-time setup)
+    step.prepare()
+    for _ in range(cache.steps_until_flush() + 1):
         step.replay()
-    cache.append(kt, vt, adapters=bank)
-    cache.decode(q, adapters=bank, out=out)
+    step.prepare()
     n = cache.steps_until_flush()
     for _ in range(3):
-        step.replay()                         # the first replay re-captures (the flush added a chunk)
+        step.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -357,15 +359,15 @@ def run_serving_loop(cache, q, bank, dev):
     torch.cuda.synchronize()
     step_us = e0.elapsed_time(e1) * 1e3 / (n - 3)
     e0.record()
-    cache.append(kt, vt, adapters=bank)      # every sequence flushes one chunk
-    cache.decode(q, adapters=bank, out=out)
+    step.replay()                            # every sequence flushes one chunk
     e1.record()
     torch.cuda.synchronize()
     flush_us = e0.elapsed_time(e1) * 1e3
     return {"graph_step_us": step_us, "flush_step_us": flush_us,
             "us_per_step_amortised": (127 * step_us + flush_us) / 128,
-            "note": "append + decode per step (steady state, second flush period); the flushing step "
-                    "(all 128 units, lockstep) runs eagerly with host launch overhead (tensor-core ring flush)"}
+            "note": "append + decode per step, one CUDA graph launch each (steady state, second flush "
+                    "period); the flushing step (all 128 units in lockstep) is a graph with the tensor-core "
+                    "ring flush (quant_kernel split over 5 CTAs per unit, flush_tc_kernel adding into S)"}
 
 
 def run_other_configs(dev, peak_gbs):

@@ -291,44 +291,96 @@ class BatchedKVCache:
 
     def capture_serving_step(self, q: torch.Tensor, k_t: torch.Tensor, v_t: torch.Tensor,
                              adapters: AdapterBank | None = None, out: torch.Tensor | None = None):
-        """One steady-state decode-loop step in one CUDA graph: append k_t, v_t (one token
-        per sequence, cache.py:120-130) then the fused decode of q.  Refill q / k_t / v_t
-        in place and call `.replay()`; each replay advances the host length mirrors and
-        refuses to run into a flush (run that step eagerly: `append` then `decode`).  The
-        decode plan depends on the chunk counts, so after a flush the next replay
-        re-captures the graph."""
+        """Decode-loop steps as CUDA graph launches: append k_t, v_t (one token per
+        sequence, cache.py:120-130) then the fused decode of q.  A step on which some
+        sequences reach R + G replays a graph that also flushes them (kvlc_append with the
+        tensor-core ring flush, cache.py:132-158).  The decode plan depends on the chunk
+        counts, so graphs are keyed by (flush mask, chunk counts) and captured on first
+        use; `.prepare()` captures the next flushing step's graph and the steady-state
+        graph after it ahead of time.  Refill q / k_t / v_t in place and call `.replay()`;
+        each replay advances the host mirrors (lengths, ring start, chunk counts)."""
         if k_t.shape != (self.B, self.Hkv, D) or v_t.shape != k_t.shape:
             raise ValueError(f"token dims {tuple(k_t.shape)}/{tuple(v_t.shape)} != ({self.B}, {self.Hkv}, {D})")
         if out is None:
             out = torch.empty(q.shape, dtype=torch.bfloat16, device=self.device)
         cache = self
+        ad_on = _adapters_on(adapters)
+        # workspaces sized once (largest plan up to capacity, the tensor-core flush) so the
+        # pointers baked into captured graphs stay valid
+        saved = cache.n_chunks
+        need = 0
+        for nc in range(int(saved.min()), cache.max_chunks + 1):
+            cache.n_chunks = np.full_like(saved, nc)
+            need = max(need, cache.decode_workspace_bytes())
+        cache.n_chunks = saved
+        dws = cache.decode_ws(need)
+        fws = cache.workspace(_lib.load().kvlc_append_workspace(ctypes.byref(cache._struct))) if ad_on else None
 
-        def capture():
-            cache.decode(q, adapters, out=out)  # sizes the decode workspace
-            torch.cuda.synchronize()
+        def due():
+            return (cache.res_len + 1 == R + G).astype(np.int32)
+
+        def capture(mask):
+            m = (tuple(mask.tolist()), tuple(cache.n_chunks.tolist()))
             ad = _adapter_struct(adapters)
             a_c = (ctypes.c_int32 * cache.B)(*([1] * cache.B))
-            f_c = (ctypes.c_int32 * cache.B)(*([0] * cache.B))
+            f_c = (ctypes.c_int32 * cache.B)(*mask.tolist())
+            tc = ad_on and np.any(mask) and getattr(cache, "_tc_flush", True)
+            saved_n = cache.n_chunks
+            torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                _lib.call("kvlc_append", ctypes.byref(cache._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
-                          a_c, f_c, None, 0, _lib.stream_handle())
-                cache.decode(q, adapters, out=out)
-            return graph, cache.n_chunks.copy()
+            try:
+                with torch.cuda.graph(graph):
+                    _lib.call("kvlc_append", ctypes.byref(cache._struct), ctypes.byref(ad), _ptr(k_t), _ptr(v_t),
+                              a_c, f_c, _ptr(fws) if tc else None, fws.numel() if tc else 0,
+                              _lib.stream_handle())
+                    cache.n_chunks = saved_n + mask   # the decode's plan: counts after this step
+                    cache.decode(q, adapters, out=out)
+            finally:
+                cache.n_chunks = saved_n
+            if cache._dws is not dws:
+                raise RuntimeError("decode workspace reallocated during capture")
+            return m, graph
 
         class _Step:
             def __init__(self):
-                self.graph, self.chunks = capture()
+                self.graphs = {}
+
+            def _graph(self, mask):
+                key = (tuple(mask.tolist()), tuple(cache.n_chunks.tolist()))
+                if key not in self.graphs:
+                    if len(self.graphs) >= 4:
+                        self.graphs.pop(next(iter(self.graphs)))
+                    k2, g = capture(mask)
+                    self.graphs[k2] = g
+                return self.graphs[key]
 
             def replay(self):
-                if cache.steps_until_flush() < 1:
-                    raise ValueError("a sequence flushes on this append: run the step eagerly")
-                if not np.array_equal(self.chunks, cache.n_chunks):  # a flush changed the plan
-                    self.graph, self.chunks = capture()
-                self.graph.replay()
-                cache.res_len = cache.res_len + 1
+                mask = due()
+                self._graph(mask).replay()
+                cache.res_len = cache.res_len + 1 - mask * G
+                cache.res_start = np.where(mask > 0, (cache.res_start + G) % SLOTS, cache.res_start)
+                cache.n_chunks = cache.n_chunks + mask
+                if ad_on:
+                    cache.state_rank[mask > 0] = RANK
 
-        return _Step(), out
+            def prepare(self):
+                """Capture (without running) the graphs of the next flushing step and of the
+                steady state right after it."""
+                saved = (cache.res_len, cache.res_start, cache.n_chunks)
+                try:
+                    steps = cache.steps_until_flush()
+                    cache.res_len = cache.res_len + steps
+                    mask = due()
+                    self._graph(mask)
+                    cache.res_len = cache.res_len + 1 - mask * G
+                    cache.n_chunks = cache.n_chunks + mask
+                    self._graph(due())
+                finally:
+                    cache.res_len, cache.res_start, cache.n_chunks = saved
+
+        step = _Step()
+        step._graph(due())
+        return step, out
 
     def decode_partial(self, q: torch.Tensor, chunk_lo: int, chunk_hi: int, include_tail: bool,
                        adapters: AdapterBank | None = None, chunks_per_split: int = 0,

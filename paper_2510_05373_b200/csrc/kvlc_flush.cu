@@ -129,6 +129,10 @@ struct FlushArgs {
   uint8_t* cimg;             // [slot][FT_TILE]  value codes as fp16, [M = channel][K = token] MN-major
   float2* vsz;               // [slot][G]  value (scale, zero) per token, fp32 (v_q = s code + z)
   int slot_stride;
+  // quant_kernel work split (decode-time ring flushes: one chunk per unit, latency-bound):
+  // 0 = one CTA per chunk does K1 and K2; n > 0 = blockIdx.z 0 does K1, z = 1..n do K2 on
+  // the tokens of 32-token slice z - 1 (n = G / 32)
+  int vsplit;
 };
 
 __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs a, const SeqInfo seq) {
@@ -733,6 +737,8 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
                       (uint32_t)__ldg(p + 2 * a.v_c) | ((uint32_t)__ldg(p + 3 * a.v_c) << 16));
   };
   const size_t slot = (size_t)unit * a.slot_stride + ci;
+  const int zpart = blockIdx.z;
+  if (zpart == 0) {
     // ---- K1: keys, channel-wise.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3
     // (16-B vector loads).  Codes in fp32 with the exact fp64 decision near rounding
     // ties (quantize.py:202-207 bit-exact); the lane also packs the fragment-native
@@ -825,25 +831,30 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         for (int t0 = 0; t0 < 4; ++t0) c.kcodes[cb * 1024 + ((wt * 32 + 4 * g + t0) * 8 + warp)] = frag_store(cw[t0]);
       }
     }
+  }
+  // token range of K2: the whole chunk, or 32-token slice zpart - 1
+  const int t_lo = a.vsplit ? (zpart - 1) * (G / a.vsplit) : 0;
+  const int ntok_w = a.vsplit ? G / a.vsplit / (FT_THREADS / 32) : G / (FT_THREADS / 32);  // per warp
+  if (a.vsplit == 0 || zpart > 0) {
     // ---- K2: values, FWHT post-rotation (fp32, guarded), token-wise quantization ----
     // The fp32 FWHT differs from the reference's fp64 dense x @ H in the last bits:
     // a token whose quotient lies near a rounding tie or whose scale / zero lies near
     // an fp16 rounding midpoint is re-evaluated in the reference's exact order.
     // rolling 8-deep register prefetch of this warp's 16 value rows (one 8-B piece per lane)
-    constexpr int VPF = 8, VTOK = G / (FT_THREADS / 32);
+    constexpr int VPF = 8;
     uint2 vpf[VPF];
 #pragma unroll
     for (int i = 0; i < VPF; ++i)
-      vpf[i] = ldv(warp + 8 * i);
+      if (i < ntok_w) vpf[i] = ldv(t_lo + warp + 8 * i);
 #pragma unroll 1
-    for (int ti = 0; ti < VTOK; ++ti) {
-      const int t = warp + 8 * ti;
+    for (int ti = 0; ti < ntok_w; ++ti) {
+      const int t = t_lo + warp + 8 * ti;
       float xf[4];
       {
         uint2 raw = vpf[0];
 #pragma unroll
         for (int i = 0; i < VPF - 1; ++i) vpf[i] = vpf[i + 1];
-        if (ti + VPF < VTOK)
+        if (ti + VPF < ntok_w)
           vpf[VPF - 1] = ldv(t + 8 * VPF);
         xf[0] = __uint_as_float(raw.x << 16);
         xf[1] = __uint_as_float(raw.x & 0xffff0000u);
@@ -995,8 +1006,11 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         c.vzero[cb * G + t] = meta_z;
       }
     }
-  __syncthreads();
-  for (int wi = tid; wi < 1024; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = frag_store(pack_v_word_sw(sm.codes, wi));
+    __syncthreads();
+    // V words of the CTA's slices (a word covers tokens of one 32-token slice: 256 words each)
+    const int w_lo = a.vsplit ? 256 * (zpart - 1) : 0, w_hi = a.vsplit ? w_lo + 256 : 1024;
+    for (int wi = w_lo + tid; wi < w_hi; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = frag_store(pack_v_word_sw(sm.codes, wi));
+  }
 }
 
 #ifdef KVLC_TRACE
@@ -1005,10 +1019,14 @@ __device__ long long g_ftrace[2][40][10];  // CTA (0, 0, h): per chunk clock64 a
   do {                                                                                         \
     if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && it < 40) g_ftrace[h][it][i] = clock64(); \
   } while (0)
+// kernel phases of CTA (0, 0, h) in slot 39: entry, setup done, chunk loop done, drain done
+#define FT_PHASE(i) \
+  do { if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_ftrace[h][39][i] = clock64(); } while (0)
 #else
 #define FT_STAMP(i) \
   do {              \
   } while (0)
+#define FT_PHASE(i) do { } while (0)
 #endif
 
 // The chunk's operand images (written by quant_kernel) into the shared-memory tiles.
@@ -1056,6 +1074,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   const int c_lo = split * a.cpc, c_hi = min(nf, c_lo + a.cpc);
   if (c_lo >= c_hi) return;
   const size_t slot0 = (size_t)unit * a.slot_stride;
+  FT_PHASE(0);
 
   // resident W_h tiles (prepared by prep_wtiles_kernel), TMEM, barriers, first images
   {
@@ -1086,6 +1105,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   // P[f] = sum_t phi[t][f], Z[f] = sum_t z_t phi[t][f] for this warp's 32 token rows:
   // lane owns features 64 part + 2 lane + {0, 1} (reduce-scatter order)
   float pacc[2] = {0.f, 0.f}, zacc[2] = {0.f, 0.f};
+  FT_PHASE(1);
 
   for (int ci = c_lo; ci < c_hi; ++ci) {
     const int it = ci - c_lo;
@@ -1186,6 +1206,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
 
   // ---- drain: S[c][h*128 + f] = D^T[c][f] + (z^T Phi)[f] (cache.py:155-157), P[h*128 + f] ----
   tc::mbar_wait(&sm.ms, (uint32_t)(c_hi - c_lo - 1) & 1u);
+  FT_PHASE(2);
   tc::fence_after_sync();
   float* zf = reinterpret_cast<float*>(sm.ps[0]);  // free now: [4 token groups][128 features][P, Z]
   {
@@ -1201,25 +1222,49 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     for (int g4 = 0; g4 < 4; ++g4) pf += zf[(g4 * 128 + tid) * 2];
     P[h * HALF + tid] += pf;
   }
+  // S rows: TMEM -> a padded shared tile (the W / A tiles are free now) -> coalesced 16-B
+  // read-modify-writes of whole S rows with the rank-1 term added (a thread per TMEM row
+  // walking its row took ~20 us per CTA: every warp access touched 32 rows, r02
+  // tools/trace_flushstep.py)
   {
+    constexpr int TLD = 132;  // floats per tile row: 16-B aligned, 4-wavefront float4 stores
+    float* tile = reinterpret_cast<float*>(sm.w[0]);            // [128 channels][TLD]
+    float* ztv = reinterpret_cast<float*>(sm.red);              // [128] (z^T Phi)[f]
+    static_assert(sizeof(sm.w) + sizeof(sm.a) >= 128 * TLD * sizeof(float), "transpose tile");
+    static_assert(sizeof(sm.red) >= 128 * sizeof(float), "z^T Phi row");
     const int cch = 32 * (warp & 3) + lane;  // TMEM lane = value channel
-    float d[32];
 #pragma unroll 1
     for (int c0 = 64 * part; c0 < 64 * part + 64; c0 += 32) {
+      float d[32];
       tc::tmem_ld32(lane_addr + FT_COL_S + c0, reinterpret_cast<uint32_t*>(d));
       tc::wait_ld();
-      float* row = S + (size_t)cch * RANK + h * HALF + c0;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int f = c0 + i;
-        const float zt = (zf[(0 * 128 + f) * 2 + 1] + zf[(1 * 128 + f) * 2 + 1]) +
-                         (zf[(2 * 128 + f) * 2 + 1] + zf[(3 * 128 + f) * 2 + 1]);
-        row[i] += d[i] + zt;
-      }
+      for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4*>(tile + cch * TLD + c0 + i) = make_float4(d[i], d[i + 1], d[i + 2], d[i + 3]);
+    }
+    if (tid < HALF) {
+      const int f = tid;
+      ztv[f] = (zf[(0 * 128 + f) * 2 + 1] + zf[(1 * 128 + f) * 2 + 1]) +
+               (zf[(2 * 128 + f) * 2 + 1] + zf[(3 * 128 + f) * 2 + 1]);
+    }
+    __syncthreads();
+#pragma unroll  // all 16 row pieces of the thread in flight at once
+    for (int idx = tid; idx < 128 * 32; idx += FT_THREADS) {
+      const int r = idx >> 5, f4 = (idx & 31) * 4;
+      const float4 t4 = *reinterpret_cast<const float4*>(tile + r * TLD + f4);
+      const float4 z4 = *reinterpret_cast<const float4*>(ztv + f4);
+      float4* dst = reinterpret_cast<float4*>(S + (size_t)r * RANK + h * HALF + f4);
+      float4 o = *dst;
+      o.x += t4.x + z4.x;
+      o.y += t4.y + z4.y;
+      o.z += t4.z + z4.z;
+      o.w += t4.w + z4.w;
+      *dst = o;
     }
   }
   tc::fence_before_sync();
   __syncthreads();
+  FT_PHASE(3);
   if (warp == 0) tc::tmem_dealloc(tb, FT_TMEM);
 }
 
@@ -1270,6 +1315,9 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
   const int waves = (2 * units * base + sms - 1) / sms;  // one CTA per SM: fill the last wave
   const int splits = std::min({ws_splits, std::max(1, max_nf), std::max(base, waves * sms / (2 * units))});
   const int cpc = (max_nf + splits - 1) / splits;
+  // one CTA per (unit, feature half): it adds its S / P straight into the cache (the halves
+  // write disjoint columns), no partials, memset or reduction (decode-time ring flushes)
+  const bool direct = splits == 1;
   Arena ar(ws, ws_bytes);
   float* s_part = ar.take<float>((size_t)units * splits * (D * RANK + RANK));
   uint8_t* wtiles = ar.take<uint8_t>((size_t)c->Hkv * 2 * 2 * FT_TILE);
@@ -1279,25 +1327,29 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
   float2* vsz = ar.take<float2>((size_t)units * slot_stride * G);
   KVLC_REQUIRE(s_part && wtiles && aimg && cimg && vsz, "flush workspace too small (%zu bytes)", ws_bytes);
   float* p_part = s_part + (size_t)units * splits * D * RANK;
-  KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
+  if (!direct) KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
   prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
   if ((rc = check_launch("prep_wtiles"))) return rc;
   a.c = *c;
   a.ad = *ad;
   a.use_adapter = 1;
   a.cpc = cpc;
-  a.s_out = s_part;
-  a.p_out = p_part;
+  a.s_out = direct ? nullptr : s_part;
+  a.p_out = direct ? nullptr : p_part;
   a.splits = splits;
   a.aimg = aimg;
   a.cimg = cimg;
   a.vsz = vsz;
   a.slot_stride = slot_stride;
-  quant_kernel<<<dim3(max_nf, units), FT_THREADS, 0, s>>>(a, seq);
+  // decode-time ring flushes (one chunk per unit, grid below one wave): the value tokens of a
+  // chunk over 4 more CTAs, keys in the first (latency, not throughput, sets that step)
+  a.vsplit = (a.ring && max_nf == 1) ? G / 32 : 0;
+  quant_kernel<<<dim3(max_nf, units, a.vsplit ? 1 + a.vsplit : 1), FT_THREADS, 0, s>>>(a, seq);
   if ((rc = check_launch("quant"))) return rc;
   KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
   flush_tc_kernel<<<dim3(splits, units, 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
   if ((rc = check_launch("flush_tc"))) return rc;
+  if (direct) return KVLC_OK;
   reduce_state_kernel<<<dim3(32, units), 256, 0, s>>>(*c, s_part, p_part, splits);
   return check_launch("reduce_state");
 }
