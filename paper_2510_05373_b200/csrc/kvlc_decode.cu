@@ -116,6 +116,7 @@ struct DecArgs {
   void* out;              // [B][Hq][D] bf16 / f32 (final output)
   float* rec_out;         // partial mode: [B][Hq][PREC] (split-KV across devices)
   int sep_combine;        // 1: the combine is combine_kernel, PDL-chained (no arrival counters)
+  int tail_fused;         // correction half h and residual half h of a unit in one task
   uint32_t* queue;        // persistent split grid: task counter (zero between launches), or null
   int ntask;              // tasks of the split grid
 };
@@ -828,6 +829,10 @@ __device__ __forceinline__ int run_task(const DecArgs& a, unsigned char* smem, i
     else
       run_corr_unit<NG>(a, unit, smrec);
 #endif
+    if (a.tail_fused) {  // the residual half h of the same unit (tail tasks: one start-up)
+      __syncthreads();
+      run_resid<NG>(a, unit, x & 1, smrec);
+    }
   } else if ((x -= ncorr) < U * a.nsq) {
     unit = x / a.nsq;
     if (WPC)
@@ -883,7 +888,7 @@ __device__ __forceinline__ void split_body(const DecArgs& a, unsigned char* smem
     griddep_launch();  // the combine kernel may be scheduled; it waits for this grid to complete
     return;
   }
-  const int per_unit = a.nsq + (a.tail ? 2 + (a.corr_on ? a.corr_split : 0) : 0);
+  const int per_unit = a.nsq + (a.tail ? (a.tail_fused ? 0 : 2) + (a.corr_on ? a.corr_split : 0) : 0);
   __syncthreads();
   if (threadIdx.x == 0) {
     griddep_wait();   // the predecessor grid (if any) has flushed: counters / q are current
@@ -1197,7 +1202,19 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   }();
   a.corr_split = corr_split_env ? corr_split_env
                                 : ((long long)p.U * (p.nsq + 1) > 148LL * split_minb(NG) ? 2 : 1);
-  int grid = p.U * p.nsq + (tail ? 2 * p.U + (p.corr_on ? a.corr_split * p.U : 0) : 0);
+  // tail tasks: correction half h + residual half h in one CTA (one start-up and q staging
+  // instead of two; both are latency-bound) when the correction runs in halves
+  static const int tailfuse_env = [] {
+    const char* e = getenv("KVLC_TAILFUSE");
+    return e ? atoi(e) : 1;
+  }();
+  // Measured (r02, same box): one-wave grids gain (config 3 B1 x 4k 16.0 -> 13.3 us, B16 x 4k
+  // 24.9 -> 21.3), multi-wave grids lose (config 2 36.8 -> 38.6, config 3 B16 x 8k 26.4 -> 31.0:
+  // the long tail tasks hold slots the splits need), so fused only when everything fits one wave
+  const bool one_wave = (long long)p.U * (p.nsq + 2) <= 148LL * split_minb(NG);
+  if (tail && p.corr_on && tailfuse_env && one_wave && !corr_split_env) a.corr_split = 2;
+  a.tail_fused = tail && p.corr_on && a.corr_split == 2 && tailfuse_env && one_wave;
+  int grid = p.U * p.nsq + (tail ? (a.tail_fused ? 0 : 2 * p.U) + (p.corr_on ? a.corr_split * p.U : 0) : 0);
   // persistent split grid (warp-per-chunk kernel, separate combine): at most one wave of
   // CTAs that take tasks from a counter.  Measured slower (config 2 split 37.0 -> 38.1 us
   // same box, r02: every task keeps its start-up and record costs, and late long tasks
