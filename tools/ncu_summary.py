@@ -39,7 +39,9 @@ for r in src[2:]:
         continue
     toks = r[isrc].strip().split()
     op = toks[1] if toks[0].startswith("@") else toks[0]
-    cnt[op.split(".")[0]] += int(r[ix] or 0)
+    if not (r[ix] or "0").replace(",", "").isdigit():  # a repeated header (multi-kernel report)
+        continue
+    cnt[op.split(".")[0]] += int((r[ix] or "0").replace(",", ""))
 total = sum(cnt.values())
 div = units or 1
 print(f"instructions {total} ({total / div:.0f} per unit)")
