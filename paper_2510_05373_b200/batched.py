@@ -85,6 +85,23 @@ def _adapter_struct(adapters):
     return adapters.struct()
 
 
+class _GuardedGraph:
+    """A captured decode step: the split plan and the decode workspace pointer
+    are fixed at capture, so replay refuses to run once the cache's chunk counts or its
+    decode workspace changed (a flush, or a later decode that grew the workspace)."""
+
+    def __init__(self, graph, cache):
+        self.graph, self.cache = graph, cache
+        self.chunks = cache.n_chunks.copy()
+        self.dws = cache._dws
+
+    def replay(self):
+        if not np.array_equal(self.chunks, self.cache.n_chunks) or self.cache._dws is not self.dws:
+            raise ValueError("the cache changed since capture_decode (chunk counts or decode workspace): "
+                             "capture again")
+        self.graph.replay()
+
+
 class BatchedKVCache:
     """Device-resident [B, Hkv] KVLinC cache (layout: include/kvlinc.h `kvlc_cache`)."""
 
@@ -283,7 +300,7 @@ class BatchedKVCache:
                 _lib.call("kvlc_stage_input", q_host.data_ptr(), q.data_ptr(), q.numel() * 2,
                           _lib.stream_handle())
             self.decode(q, adapters, literal, out, chunks_per_split)
-        return graph, out
+        return _GuardedGraph(graph, self), out
 
     def steps_until_flush(self) -> int:
         """Appends every sequence can take before one of them reaches R + G (flushes)."""

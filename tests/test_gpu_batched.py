@@ -424,3 +424,19 @@ def test_decode_right_after_prefill_from_another_thread():
     ref = oracle_decode(q, oracle_caches(k, v, [n] * B, oads), oads)
     for out in outs:
         assert np.abs(out.cpu().numpy() - ref).max() <= 1e-3 * np.abs(ref).max()
+
+
+def test_captured_decode_refuses_a_changed_cache():
+    """ADVICE r01: a capture_decode graph fixes the split plan and the workspace pointer;
+    after a flush changes the chunk counts its replay raises instead of skipping chunks."""
+    B, Hkv, Hq = 1, 1, 4
+    k, v, q = make_inputs(B, Hkv, Hq, 255, seed=51)
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=1024)
+    cache.prefill(tdev(k), tdev(v), adapters=bank)
+    g, _ = cache.capture_decode(tdev(q), adapters=bank)
+    g.replay()
+    cache.append(tdev(k[:, :, :1]).reshape(B, Hkv, D), tdev(v[:, :, :1]).reshape(B, Hkv, D), adapters=bank)
+    assert int(cache.n_chunks[0]) == 1   # 256 tokens: the append flushed a chunk
+    with pytest.raises(ValueError, match="capture again"):
+        g.replay()
