@@ -633,7 +633,7 @@ __device__ __forceinline__ void warp_fwht128(float (&x)[4], int lane) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float o = __shfl_xor_sync(0xffffffffu, x[e], k);
-      x[e] = (lane & k) ? (o - x[e]) : (x[e] + o);
+      x[e] = fmaf(x[e], (lane & k) ? -1.f : 1.f, o);  // o - x or x + o, one FFMA (exact)
     }
   }
 }

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           double o = __shfl_xor_sync(0xffffffffu, x[e], k);
-          x[e] = (lane & k) ? (o - x[e]) : (x[e] + o);
+          x[e] = fma(x[e], (lane & k) ? -1.0 : 1.0, o);  // o - x or x + o (exact)
         }
       }
       const double hs = 1.0 / sqrt((double)D);
@@ -871,7 +871,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float o = __shfl_xor_sync(0xffffffffu, xf[e], k);
-          xf[e] = (lane & k) ? (o - xf[e]) : (xf[e] + o);
+          xf[e] = fmaf(xf[e], (lane & k) ? -1.f : 1.f, o);  // o - x or x + o, one FFMA (exact)
         }
       }
       const float hsf = 0.08838834764831845f;
@@ -937,7 +937,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const double o = __shfl_xor_sync(0xffffffffu, y[e], k);
-            y[e] = (lane & k) ? (o - y[e]) : (y[e] + o);
+            y[e] = fma(y[e], (lane & k) ? -1.0 : 1.0, o);  // o - x or x + o (exact)
           }
         }
         double mn = INFINITY, mx = -INFINITY;
