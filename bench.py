@@ -377,7 +377,8 @@ def run_other_configs(dev, peak_gbs):
     kvlc_prefill (quantize/pack + FWHT + adapter-state update) of Qwen3-8B shapes."""
     import torch
     from paper_2510_05373_b200.batched import AdapterBank, BatchedKVCache, flush_count
-    out = {"config3_qwen2.5-7b_b16_ctx8k": _decode_point(dev, 16, 4, 28, 8192, peak_gbs),
+    out = {"config1_tiny_b1_8heads_ctx1k": _decode_point(dev, 1, 8, 8, 1024, peak_gbs),
+           "config3_qwen2.5-7b_b16_ctx8k": _decode_point(dev, 16, 4, 28, 8192, peak_gbs),
            "config4_llama3-8b_b1_ctx128k": _decode_point(dev, 1, 8, 32, 131072, peak_gbs)}
     sweep = {}
     for b, n in ((1, 4096), (16, 4096), (64, 4096), (1, 32768), (16, 32768), (64, 32768)):
@@ -587,6 +588,28 @@ def _oracle_unit_worker(args):
         return times
 
 
+def _config1_worker():
+    """BASELINE config 1 on one core: 8 (b, kv-head) units of 1024 tokens (MHA), one decode each."""
+    from threadpoolctl import threadpool_limits
+    import numpy as np
+    from oracle import kvlinc_oracle as orc
+    with threadpool_limits(1):
+        g = orc.rng(11)
+        units = []
+        for h in range(8):
+            k = g.standard_normal((1024, D)).astype(np.float32).astype(np.float64)
+            v = g.standard_normal((1024, D)).astype(np.float32).astype(np.float64)
+            ad = orc.init_adapter(D, RANK, seed=h)
+            units.append((orc.build_cache(k, v, ad), ad, g.standard_normal(D)))
+        times = []
+        for _ in range(3):
+            t = time.perf_counter()
+            for c, ad, qv in units:
+                orc.decode_blocked(qv, c, ad)
+            times.append(time.perf_counter() - t)
+    return statistics.median(times)
+
+
 def cpu_baseline_sample():
     """Single-core sample: one kv unit (4 q-heads) of the workload, extrapolated
     to the full step (B*Hkv = 128 units); the O(N) value-slicing port (median of 3) and,
@@ -594,6 +617,7 @@ def cpu_baseline_sample():
     cache.py:110, O(N^2 / G); identical outputs)."""
     t_unit = statistics.median(_oracle_unit_worker((0, 3, 7)))
     t_asis = _oracle_unit_worker((0, 1, 7, True))[0]
+    t_c1 = _config1_worker()
     step_s = t_unit * B * HKV
     return {"value": B / step_s, "unit": "tokens/s", "cores": 1, "kind": "port",
             "sample": f"1 of {B * HKV} (b, kv-head) units, {HQ // HKV} q-heads, ctx {CTX}, "
@@ -602,7 +626,10 @@ def cpu_baseline_sample():
             "ms_per_step": step_s * 1e3,
             "as_is": {"value": B / (t_asis * B * HKV), "unit": "tokens/s", "ms_per_unit": t_asis * 1e3,
                       "sample": "same unit, the reference's whole-store value dequantization per block "
-                                "(cache.py:110), 1 run"}}
+                                "(cache.py:110), 1 run"},
+            "config1": {"ms_per_step": t_c1 * 1e3, "unit": "ms per decode step", "cores": 1,
+                        "sample": "BASELINE config 1 whole step: B1, 8 MHA heads, ctx 1024, oracle "
+                                  "decode_step_blocked per head, median of 3"}}
 
 
 def run_reference(args, world):

@@ -254,6 +254,17 @@ int kvlc_decode(const kvlc_cache* cache, const kvlc_adapter* ad,
                 const uint16_t* q, void* out, const kvlc_decode_opts* o,
                 void* ws, size_t ws_bytes, void* stream);
 
+/* decode_step_blocked(..., return_partials=True) at block_tokens = G on the serving cache
+ * (attention.py:41-47, 197-276): the fused decode (out as kvlc_decode) plus, per (b, q-head),
+ * its per-block partials in blocks [B][Hq][max_blocks][2 + 128] fp32 = (block max m in natural
+ * logit units, block sum l = sum exp(s - m), y = sum exp(s - m) v in the stored basis): the
+ * n_chunks[b] quantized blocks, then the residual window as one block; rows past a sequence's
+ * blocks are zero.  max_blocks >= max n_chunks + 1.  Workspace: kvlc_decode_workspace() with
+ * chunks_per_split = 1. */
+int kvlc_decode_blocks(const kvlc_cache* cache, const kvlc_adapter* ad, const uint16_t* q,
+                       void* out, float* blocks, int32_t max_blocks, const kvlc_decode_opts* o,
+                       void* ws, size_t ws_bytes, void* stream);
+
 /* Marks `cache` as written outside this library (codes, metadata or chunk counts):
  * its next decode launches without overlapping the preceding kernel. */
 void kvlc_note_cache_write(const kvlc_cache* cache);

@@ -1069,6 +1069,52 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
   finish(M, Mt, den, nr, nw, corr ? cbuf : nullptr, literal, lane, o, out_fp32);
 }
 
+// Per-block partials of decode_step_blocked (return_partials, attention.py:41-47, 269-275) from
+// the records of a one-chunk-per-split decode: block i < n_chunks (the quantized blocks of
+// G tokens, stored basis) and one residual block (the two ring halves merged), converted from
+// the kernel's log2-unit reference points to the reference's natural-unit block max:
+// m = m_true ln 2, l and y scaled by 2^(m_ref - m_true).  out: [B][Hq][max_blocks][2 + D].
+__global__ void __launch_bounds__(128) blocks_kernel(const kvlc_cache c, const float* __restrict__ rec, int nrec,
+                                                     int nsq, int NG, int max_blocks, float* __restrict__ out) {
+  const int gw = blockIdx.x, b = gw / c.Hq, qh = gw % c.Hq, kvh = qh / NG, hl = qh % NG;
+  const int unit = b * c.Hkv + kvh;
+  const int nq = min(c.n_chunks[b], nsq), has_res = c.res_len[b] > 0 ? 1 : 0;
+  const size_t rs = (size_t)NG * REC;
+  const float* base = rec + ((size_t)unit * nrec * NG + hl) * REC;
+  float* o = out + (size_t)gw * max_blocks * (2 + D);
+  const float LN2 = 0.6931471805599453f;
+  for (int i = 0; i < max_blocks; ++i) {
+    float m = 0.f, l = 0.f, f0 = 0.f, f1 = 0.f;
+    const float *y0 = nullptr, *y1 = nullptr;
+    if (i < nq) {
+      const float* r = base + i * rs;
+      f0 = r[2] == -INFINITY ? 0.f : exp2f(r[0] - r[2]);
+      m = r[2] * LN2;
+      l = r[1] * f0;
+      y0 = r + 4;
+    } else if (i == nq && has_res) {
+      const float* r0 = base + nsq * rs;
+      const float* r1 = base + (nsq + 1) * rs;
+      const float M = fmaxf(r0[2], r1[2]);
+      f0 = r0[0] == -INFINITY ? 0.f : exp2f(r0[0] - M);
+      f1 = r1[0] == -INFINITY ? 0.f : exp2f(r1[0] - M);
+      m = M * LN2;
+      l = r0[1] * f0 + r1[1] * f1;
+      y0 = r0 + 4;
+      y1 = r1 + 4;
+    }
+    if (threadIdx.x == 0) {
+      o[i * (2 + D)] = m;
+      o[i * (2 + D) + 1] = l;
+    }
+    const int ch = threadIdx.x;
+    float y = 0.f;
+    if (y0) y = y0[ch] * f0;
+    if (y1) y = fmaf(y1[ch], f1, y);
+    o[i * (2 + D) + 2 + ch] = y;
+  }
+}
+
 // ------------------------------------------------------------- host ----
 // Quantized splits warp per chunk or warp per 32-token slice.  Same-box A/B (r02,
 // tools/run_var.sh): config 2 (4 heads per group) 37.0 vs 36.8 us, config 4 29.7 vs 33.5 us,
@@ -1335,6 +1381,27 @@ int kvlc_decode(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, 
   KVLC_REQUIRE(ws && ws_bytes >= p.total, "decode workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
   return launch(c, ad, q, p, static_cast<char*>(ws), 0, 1 << 30, 1, nullptr, o ? o->literal : 0,
                 o ? o->out_fp32 : 0, out, nullptr, o, as_stream(stream));
+}
+
+int kvlc_decode_blocks(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, void* out, float* blocks,
+                       int32_t max_blocks, const kvlc_decode_opts* o, void* ws, size_t ws_bytes, void* stream) {
+  KVLC_NEED_DEVICE();
+  KVLC_REQUIRE(q && out && blocks, "null query / output / blocks");
+  kvlc_decode_opts o1{};
+  if (o) o1 = *o;
+  o1.chunks_per_split = 1;  // one record per quantized chunk = one block of G tokens
+  Plan p{};
+  int rc = plan_for(c, &o1, 0, 1 << 30, 1, adapter_active(ad), p);
+  if (rc) return rc;
+  KVLC_REQUIRE(ws && ws_bytes >= p.total, "decode workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
+  KVLC_REQUIRE(max_blocks >= p.nsq + 1, "blocks buffer holds %d blocks per head, the cache needs %d", max_blocks,
+               p.nsq + 1);
+  rc = launch(c, ad, q, p, static_cast<char*>(ws), 0, 1 << 30, 1, nullptr, o1.literal, o1.out_fp32, out, nullptr, &o1,
+              as_stream(stream));
+  if (rc) return rc;
+  blocks_kernel<<<c->B * c->Hq, 128, 0, as_stream(stream)>>>(
+      *c, reinterpret_cast<const float*>(static_cast<char*>(ws) + p.rec_off), p.nrec, p.nsq, p.NG, max_blocks, blocks);
+  return check_launch("decode_blocks");
 }
 
 int kvlc_decode_partial(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q,

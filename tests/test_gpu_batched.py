@@ -440,3 +440,34 @@ def test_captured_decode_refuses_a_changed_cache():
     assert int(cache.n_chunks[0]) == 1   # 256 tokens: the append flushed a chunk
     with pytest.raises(ValueError, match="capture again"):
         g.replay()
+
+
+@pytest.mark.parametrize("Hq", [4, 8])
+def test_decode_blocks_match_reference_partials(Hq):
+    """return_partials on the serving cache (kvlc_decode_blocks, block_tokens = G): per-block
+    (max, sum, y) against decode_step_blocked's DecodePartial on the oracle cache."""
+    B, Hkv, n = 2, 2, 900
+    lens = [900, 700]
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=61)
+    oads = [orc.init_adapter(D, 256, seed=h) for h in range(Hkv)]
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k), tdev(v), lens=lens, adapters=bank)
+    out, part = cache.decode_blocks(tdev(q), adapters=bank)
+    full = cache.decode(tdev(q), adapters=bank, out_dtype=F32)
+    assert (out - full).abs().max().item() <= 2e-4 * full.abs().max().item()
+    ocs = oracle_caches(k, v, lens, oads)
+    NG = Hq // Hkv
+    for b in range(B):
+        nbk = int(part["n_blocks"][b])
+        for h in range(Hq):
+            oc = orc.fp16_meta_copy(ocs[b][h // NG])
+            _, (ry, rm, rl) = orc.decode_blocked(q[b, h].astype(np.float64), oc, oads[h // NG], return_partials=True)
+            assert len(rm) == nbk
+            m = part["m"][b, h, :nbk].cpu().numpy()
+            l = part["l"][b, h, :nbk].cpu().numpy()
+            y = part["y"][b, h, :nbk].cpu().numpy()
+            assert np.abs(m - rm).max() <= 1e-4 * max(1.0, np.abs(rm).max()), (b, h)
+            assert np.abs(l - rl).max() <= 2e-4 * np.abs(rl).max(), (b, h)
+            assert np.abs(y - ry).max() <= 1e-3 * np.abs(ry).max(), (b, h)
+            assert not part["y"][b, h, nbk:].any()
