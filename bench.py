@@ -384,6 +384,7 @@ def run_other_configs(dev, peak_gbs):
     for b, n in ((1, 4096), (16, 4096), (64, 4096), (1, 32768), (16, 32768), (64, 32768)):
         sweep[f"b{b}_ctx{n // 1024}k"] = _decode_point(dev, b, 4, 28, n, peak_gbs)
     out["config3_sweep_qwen2.5-7b"] = sweep
+    out["prefill_corrected_attention"] = run_prefill_attention(dev, peak_gbs)
     # config 5: prefill of 32k tokens x 8 kv heads (Qwen3-8B attention shapes)
     b, hkv, n = 1, 8, 32768
     bank = AdapterBank.initialize(hkv, device=dev)
@@ -502,6 +503,40 @@ def run_multi_gpu(args, rank, world, dev, peak_gbs):
         "collective": "one NCCL all_gather per step of [record | correction] (B x Hq x 389 fp32 per rank)",
         "out_finite": bool(torch.isfinite(o).all().item())}
     return out
+
+
+def run_prefill_attention(dev, peak_gbs):
+    """Corrected causal prefill attention (attention.py:99-155) on the
+    tensor cores: 8 heads x 8192 tokens with rank-256 adapters (kvlc_corrected_attention, the
+    fp16 operand images included; phi_q / phi_k precomputed outside the timed region)."""
+    import torch
+    from paper_2510_05373_b200 import _lib
+    heads, n = 8, 8192
+    g = torch.Generator(device=dev).manual_seed(5)
+    q, k, v = (torch.randn(heads, n, D, device=dev, generator=g) for _ in range(3))
+    ph = [torch.softmax(torch.randn(heads, n, 2, 128, device=dev, generator=g), -1).reshape(heads, n, 256)
+          for _ in range(2)]
+    out = torch.empty_like(q)
+    ws = torch.empty(_lib.load().kvlc_corrected_attention_workspace(n, heads, 256), dtype=torch.uint8, device=dev)
+
+    def call():
+        _lib.call("kvlc_corrected_attention", q.data_ptr(), k.data_ptr(), v.data_ptr(), ph[0].data_ptr(),
+                  ph[1].data_ptr(), n, heads, 256, out.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle())
+
+    call()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    pairs = heads * n * (n + 1) / 2
+    flops = pairs * 2 * (D + RANK + D)   # q.k, phi_q.phi_k, w.v once each
+    return {"us_per_step": ms * 1e3, "heads": heads, "tokens": n, "adapter_rank": RANK,
+            "tflops_algorithmic": flops / (ms * 1e-3) / 1e12,
+            "kernel": "pa_kernel (mma.sync m16n8k16, fp16 hi/lo q/k/v in 3 passes, phi in 1 pass, fp32 accumulate)"}
 
 
 def run_flash_attn(args, dev, ours_ms):

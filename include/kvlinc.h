@@ -104,6 +104,19 @@ int kvlc_ref_attention(const double* q, const double* k, const double* v, int64_
                        int d, const double* phq, const double* phk, int rank,
                        int shifted, double* weights, double* out, void* stream);
 
+/* Corrected causal prefill attention, fast path (attention.py:99-155: the quadratic and
+ * recurrent forms give the same outputs): for every head and query t,
+ *   out_t = sum_{i<=t} (e^{q_t.k_i/sqrt(128)} + phq_t . phk_i) v_i / sum_{i<=t} (...)
+ * q, k (the dequantized keys), v (dequantized values), out: fp32 [heads][n][128];
+ * phq = phi_q(q), phk = phi_k(k_err): fp32 [heads][n][256] (rank 256), or rank 0 and NULL
+ * (no adapter).  Tensor cores (mma.sync, fp16 hi / lo operands, fp32 accumulation); the
+ * exponentials are shifted by max(0, running max) with the correction scaled alike.
+ * Workspace: kvlc_corrected_attention_workspace(n, heads, rank) bytes. */
+size_t kvlc_corrected_attention_workspace(int64_t n, int heads, int rank);
+int kvlc_corrected_attention(const float* q, const float* k, const float* v, const float* phq,
+                             const float* phk, int64_t n, int heads, int rank, float* out,
+                             void* ws, size_t ws_bytes, void* stream);
+
 /* One flush of a per-head cache (cache.py:132-158): the oldest `group`
  * residual tokens k_blk/v_blk [group][d] are quantized (keys channel-wise,
  * values optionally post-rotated then token-wise) and, when w1k != NULL, the

@@ -50,6 +50,9 @@ _SIGS = {
     "kvlc_last_error": (ctypes.c_char_p, []),
     "kvlc_device_ok": (c_int, []),
     "kvlc_note_cache_write": (None, [POINTER(KvlcCache)]),
+    "kvlc_corrected_attention_workspace": (c_size_t, [c_int64, c_int, c_int]),
+    "kvlc_corrected_attention": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int,
+                                         c_void_p, c_void_p, c_size_t, c_void_p]),
     "kvlc_decode_blocks": (c_int, [POINTER(KvlcCache), POINTER(KvlcAdapter), c_void_p, c_void_p, c_void_p,
                                    c_int32, POINTER(KvlcDecodeOpts), c_void_p, c_size_t, c_void_p]),
     "kvlc_ref_pack": (c_int, [c_void_p, c_int64, c_int64, c_int, c_void_p, c_void_p]),
