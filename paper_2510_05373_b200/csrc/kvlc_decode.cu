@@ -117,6 +117,8 @@ struct DecArgs {
   float* rec_out;         // partial mode: [B][Hq][PREC] (split-KV across devices)
   int sep_combine;        // 1: the combine is combine_kernel, PDL-chained (no arrival counters)
   int tail_fused;         // correction half h and residual half h of a unit in one task
+  int rps;                // records per quantized split: 1 (CTA-merged) or 4 (one per warp)
+  int qrec;               // quantized records per unit (nsq * rps); residual records follow
   uint32_t* queue;        // persistent split grid: task counter (zero between launches), or null
   int ntask;              // tasks of the split grid
 };
@@ -269,7 +271,7 @@ __device__ __forceinline__ void run_resid(const DecArgs& a, int unit, int hf, fl
   }
   warp_store<NG, false>(st, smrec + warp * NG * REC, lane);
   __syncthreads();
-  cta_merge<NG>(smrec, a.rec + ((size_t)unit * a.nrec + a.nsq + hf) * NG * REC);
+  cta_merge<NG>(smrec, a.rec + ((size_t)unit * a.nrec + a.qrec + hf) * NG * REC);
 }
 
 // Correction of one unit by one CTA (both feature halves; used when the splits and these
@@ -778,7 +780,7 @@ __device__ __forceinline__ void combine_head(const DecArgs& a, int NG, int b, in
         for (int u = 0; u < CB; ++u) {
           const int i = i0 + u;
           if (i >= cnt) break;
-          float* acc = r0 + i < a.nsq ? nr : nw;  // warp-uniform: quantized (rotated) vs residual (raw) basis
+          float* acc = r0 + i < a.qrec ? nr : nw;  // warp-uniform: quantized (rotated) vs residual (raw) basis
           acc[0] = fmaf(wv[u], y[u].x, acc[0]);
           acc[1] = fmaf(wv[u], y[u].y, acc[1]);
           acc[2] = fmaf(wv[u], y[u].z, acc[2]);
@@ -982,7 +984,7 @@ __global__ void __launch_bounds__(THREADS) combine_kernel(const DecArgs a) {
       const int r = warp + WARPS * i;
       if (r >= nrec) break;
       const float w = hm[r];
-      float* acc = r < a.nsq ? nr : nw;  // quantized (rotated) vs residual (raw) basis
+      float* acc = r < a.qrec ? nr : nw;  // quantized (rotated) vs residual (raw) basis
       acc[0] = fmaf(w, y[i].x, acc[0]);
       acc[1] = fmaf(w, y[i].y, acc[1]);
       acc[2] = fmaf(w, y[i].z, acc[2]);
@@ -1075,7 +1077,7 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
 // the kernel's log2-unit reference points to the reference's natural-unit block max:
 // m = m_true ln 2, l and y scaled by 2^(m_ref - m_true).  out: [B][Hq][max_blocks][2 + D].
 __global__ void __launch_bounds__(128) blocks_kernel(const kvlc_cache c, const float* __restrict__ rec, int nrec,
-                                                     int nsq, int NG, int max_blocks, float* __restrict__ out) {
+                                                     int nsq, int rps, int NG, int max_blocks, float* __restrict__ out) {
   const int gw = blockIdx.x, b = gw / c.Hq, qh = gw % c.Hq, kvh = qh / NG, hl = qh % NG;
   const int unit = b * c.Hkv + kvh;
   const int nq = min(c.n_chunks[b], nsq), has_res = c.res_len[b] > 0 ? 1 : 0;
@@ -1087,14 +1089,14 @@ __global__ void __launch_bounds__(128) blocks_kernel(const kvlc_cache c, const f
     float m = 0.f, l = 0.f, f0 = 0.f, f1 = 0.f;
     const float *y0 = nullptr, *y1 = nullptr;
     if (i < nq) {
-      const float* r = base + i * rs;
+      const float* r = base + (size_t)i * rps * rs;  // one chunk per split: warp 0's record
       f0 = r[2] == -INFINITY ? 0.f : exp2f(r[0] - r[2]);
       m = r[2] * LN2;
       l = r[1] * f0;
       y0 = r + 4;
     } else if (i == nq && has_res) {
-      const float* r0 = base + nsq * rs;
-      const float* r1 = base + (nsq + 1) * rs;
+      const float* r0 = base + (size_t)nsq * rps * rs;
+      const float* r1 = r0 + rs;
       const float M = fmaxf(r0[2], r1[2]);
       f0 = r0[0] == -INFINITY ? 0.f : exp2f(r0[0] - M);
       f1 = r1[0] == -INFINITY ? 0.f : exp2f(r1[0] - M);
@@ -1130,7 +1132,7 @@ bool wpc_on(int ng) {
 int split_minb(int ng) { return wpc_on(ng) ? wpc_minb(ng) : KVLC_SPLIT_MINB; }
 
 struct Plan {
-  int NG, U, nsq, cpc, nrec, corr_on;
+  int NG, U, nsq, cpc, nrec, corr_on, rps, qrec;
   size_t done_off, corr_off, rec_off, total;
 };
 
@@ -1187,7 +1189,15 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
   p.cpc = cpc;
   p.nsq = std::max(1, (span + cpc - 1) / cpc);
   p.corr_on = corr_on && tail ? 1 : 0;
-  p.nrec = p.nsq + (tail ? 2 : 0);
+  // warp-per-chunk splits write one record per warp (no CTA merge) while the combine can
+  // hold them all (KVLC_WARPREC=0: CTA-merged records, A/B)
+  static const int warprec_env = [] {
+    const char* e = getenv("KVLC_WARPREC");
+    return e ? atoi(e) : 1;
+  }();
+  p.rps = (warprec_env && wpc_on(p.NG) && 4 * p.nsq + (tail ? 2 : 0) <= 64) ? 4 : 1;
+  p.qrec = p.nsq * p.rps;
+  p.nrec = p.qrec + (tail ? 2 : 0);
   size_t BH = (size_t)c->B * c->Hq;
   p.corr_off = 0;
   p.rec_off = align_up(2 * BH * (1 + D) * sizeof(float));  // correction partials of the 2 halves
@@ -1219,6 +1229,8 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   a.corr_ext = corr_ext;
   a.rec = rec;
   a.nsq = p.nsq;
+  a.rps = p.rps;
+  a.qrec = p.qrec;
   a.cpc = p.cpc;
   a.chunk_lo = chunk_lo;
   a.chunk_hi = chunk_hi;
@@ -1400,7 +1412,8 @@ int kvlc_decode_blocks(const kvlc_cache* c, const kvlc_adapter* ad, const uint16
               as_stream(stream));
   if (rc) return rc;
   blocks_kernel<<<c->B * c->Hq, 128, 0, as_stream(stream)>>>(
-      *c, reinterpret_cast<const float*>(static_cast<char*>(ws) + p.rec_off), p.nrec, p.nsq, p.NG, max_blocks, blocks);
+      *c, reinterpret_cast<const float*>(static_cast<char*>(ws) + p.rec_off), p.nrec, p.nsq, p.rps, p.NG, max_blocks,
+      blocks);
   return check_launch("decode_blocks");
 }
 

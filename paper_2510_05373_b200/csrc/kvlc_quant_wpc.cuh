@@ -364,6 +364,11 @@ __device__ __forceinline__ void run_quant_wpc(const DecArgs& a, int unit, int sp
     for (int s = 0; s < WPC_RING; ++s)
       asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(tc::smem_u32(&q.full[warp][s])) : "memory");
   }
+  if (a.rps == 4) {  // one record per warp, straight to global memory: no CTA barrier or merge
+    __syncwarp();
+    warp_store<NG, true>(st, a.rec + ((size_t)unit * a.nrec + 4 * split + warp) * NG * REC, lane);
+    return;
+  }
   __syncthreads();
   PH_STAMP(2);
   warp_store<NG, true>(st, rec_sm + warp * NG * REC, lane);
