@@ -4,8 +4,12 @@
 Workload (BASELINE config 2, the headline): Llama-3-8B attention shapes,
 batch 16 per GPU, 32 q / 8 kv heads, d = 128, context 8192, 2-bit KVLinC cache
 (G = R = 128, D = 256 random-init adapter per kv head), synthetic bf16 data.
-A step = one fused decode (Algorithm 1) for every (sequence, q-head):
-phi_q prologue + split-KV kernel + LSE combine.
+A step = one fused decode (Algorithm 1) for every (sequence, q-head): the split
+kernel (correction CTAs incl. phi_q, warp-per-chunk quantized splits streaming 2-bit
+chunks by TMA, residual halves) + the LSE combine, PDL-chained, one CUDA graph launch.
+The same JSON line carries configs 1 and 3-5, the config-3 sweep, the corrected prefill
+attention, the serving loop, bf16 FlashAttention-2 / FlashInfer, the e2e (host in / out)
+number and a CPU sample of the reference algorithm.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -259,9 +263,9 @@ def run_ours(args, rank, world, local_rank):
                         "host memory; one CUDA graph launch per step (3 kernels, PDL-chained)",
                 "gpu_launches": 3 * K},
         "gpu_launches": 2 * K,
-        "launch": "CUDA graph per step: split_kernel (correction CTAs incl. phi_q, quantized splits "
-                  "streaming whole chunks by TMA bulk copies, residual halves) + combine_kernel "
-                  "(LSE merge per (b, q-head)), chained by programmatic dependent launch",
+        "launch": "CUDA graph per step: split_kernel_wpc (correction CTAs incl. phi_q, warp-per-chunk "
+                  "quantized splits streaming K / V half-chunks by TMA bulk copies, residual halves) + "
+                  "combine_kernel (LSE merge per (b, q-head)), chained by programmatic dependent launch",
         "clocks": clk.summary(),
     }
     if multi is not None:
