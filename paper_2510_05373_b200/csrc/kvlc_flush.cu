@@ -1008,7 +1008,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
     }
     __syncthreads();
     // V words of the CTA's slices (a word covers tokens of one 32-token slice: 256 words each)
-    const int w_lo = a.vsplit ? 256 * (zpart - 1) : 0, w_hi = a.vsplit ? w_lo + 256 : 1024;
+    const int w_lo = a.vsplit ? (zpart - 1) * (1024 / a.vsplit) : 0, w_hi = a.vsplit ? w_lo + 1024 / a.vsplit : 1024;
     for (int wi = w_lo + tid; wi < w_hi; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = frag_store(pack_v_word_sw(sm.codes, wi));
   }
 }
@@ -1343,7 +1343,16 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
   a.slot_stride = slot_stride;
   // decode-time ring flushes (one chunk per unit, grid below one wave): the value tokens of a
   // chunk over 4 more CTAs, keys in the first (latency, not throughput, sets that step)
-  a.vsplit = (a.ring && max_nf == 1) ? G / 32 : 0;
+  static const int vsplit_env = [] {
+    const char* e = getenv("KVLC_VSPLIT");
+    return e ? atoi(e) : -1;
+  }();
+  // value CTAs per chunk: enough that K1 (the key CTA) sets the time, few enough that key and
+  // value CTAs fit one wave of quant_kernel's 3 CTAs per SM
+  int vs = 4;
+  while (vs > 1 && (long long)units * (1 + vs) > 3LL * sms) vs >>= 1;
+  if (vsplit_env >= 0) vs = vsplit_env;
+  a.vsplit = (a.ring && max_nf == 1 && vs > 0) ? vs : 0;
   quant_kernel<<<dim3(max_nf, units, a.vsplit ? 1 + a.vsplit : 1), FT_THREADS, 0, s>>>(a, seq);
   if ((rc = check_launch("quant"))) return rc;
   KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
