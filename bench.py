@@ -389,6 +389,7 @@ def run_other_configs(dev, peak_gbs):
         sweep[f"b{b}_ctx{n // 1024}k"] = _decode_point(dev, b, 4, 28, n, peak_gbs)
     out["config3_sweep_qwen2.5-7b"] = sweep
     out["prefill_corrected_attention"] = run_prefill_attention(dev, peak_gbs)
+    out["adapter_train_step"] = run_train_step(dev)
     # config 5: prefill of 32k tokens x 8 kv heads (Qwen3-8B attention shapes)
     b, hkv, n = 1, 8, 32768
     bank = AdapterBank.initialize(hkv, device=dev)
@@ -507,6 +508,46 @@ def run_multi_gpu(args, rank, world, dev, peak_gbs):
         "collective": "one NCCL all_gather per step of [record | correction] (B x Hq x 389 fp32 per rank)",
         "out_finite": bool(torch.isfinite(o).all().item())}
     return out
+
+
+def run_train_step(dev):
+    """One adapter-calibration step (adapter.py:180-251) in float64 repo
+    kernels: the batched loss / gradients over 64 query positions sharing 4096 keys
+    (kvlc_adapter_grads) and Adam on the four weights (kvlc_adam_step)."""
+    import torch
+    from paper_2510_05373_b200 import _lib
+    n, b, d, rank = 4096, 64, 128, 256
+    g = torch.Generator(device=dev).manual_seed(9)
+    f64 = lambda *sh: torch.randn(*sh, device=dev, generator=g, dtype=torch.float64)
+    a = torch.softmax(f64(n, n).tril(), -1).contiguous()
+    q, kh, ke = f64(n, d), f64(n, d), 0.1 * f64(n, d)
+    w = [0.09 * f64(d, rank // 2) for _ in range(4)]
+    gr = [torch.empty_like(x) for x in w]
+    m = [torch.zeros_like(x) for x in w]
+    v2 = [torch.zeros_like(x) for x in w]
+    pos = torch.sort(torch.randperm(n, device=dev, generator=g)[:b].int())[0]
+    loss = torch.empty(1, dtype=torch.float64, device=dev)
+    ws = torch.empty(_lib.load().kvlc_adapter_grads_workspace(n, b, d, rank), dtype=torch.uint8, device=dev)
+
+    def step(t):
+        _lib.call("kvlc_adapter_grads", a.data_ptr(), q.data_ptr(), kh.data_ptr(), ke.data_ptr(), n, d, pos.data_ptr(),
+                  b, *[x.data_ptr() for x in w], rank, *[x.data_ptr() for x in gr], loss.data_ptr(), ws.data_ptr(),
+                  ws.numel(), _lib.stream_handle())
+        for i in range(4):
+            _lib.call("kvlc_adam_step", w[i].data_ptr(), m[i].data_ptr(), v2[i].data_ptr(), gr[i].data_ptr(),
+                      w[i].numel(), 0.01, 0.9, 0.999, 1e-8, t, _lib.stream_handle())
+
+    step(1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(2, 7):
+        step(t)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    return {"us_per_step": ms * 1e3, "keys": n, "positions": b, "head_dim": d, "rank": rank, "dtype": "f64",
+            "kernels": "feature maps, pa_rows_kernel, gemm_f64_kernel x6, softmax_bwd_kernel x2, adam_kernel x4"}
 
 
 def run_prefill_attention(dev, peak_gbs):

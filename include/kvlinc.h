@@ -117,6 +117,23 @@ int kvlc_corrected_attention(const float* q, const float* k, const float* v, con
                              const float* phk, int64_t n, int heads, int rank, float* out,
                              void* ws, size_t ws_bytes, void* stream);
 
+/* Adapter calibration, the trainer's inner loop (adapter.py:180-251), float64 device
+ * arrays: for query positions pos[b] (int32) sharing keys 0..n-1 with the causal mask,
+ * the batched corrected-row cross-entropy (loss, one double) and its gradients
+ * g1q/g2q/g1k/g2k [d][rank/2] for the weights w1q/w2q/w1k/w2k [d][rank/2]
+ * (_batched_loss_and_grads).  a_full [n][n] full-precision attention rows, q / khat /
+ * kerr [n][d].  Workspace: kvlc_adapter_grads_workspace(n, b, d, rank) bytes. */
+size_t kvlc_adapter_grads_workspace(int64_t n, int b, int d, int rank);
+int kvlc_adapter_grads(const double* a_full, const double* q, const double* khat,
+                       const double* kerr, int64_t n, int d, const int32_t* pos, int b,
+                       const double* w1q, const double* w2q, const double* w1k,
+                       const double* w2k, int rank, double* g1q, double* g2q, double* g1k,
+                       double* g2k, double* loss, void* ws, size_t ws_bytes, void* stream);
+/* AdamState.step (adapter.py:230-251) on one weight tensor in place: moments m, v, step
+ * count `step` (>= 1) for the bias correction. */
+int kvlc_adam_step(double* w, double* m, double* v, const double* g, int64_t count, double lr,
+                   double beta1, double beta2, double eps, int64_t step, void* stream);
+
 /* One flush of a per-head cache (cache.py:132-158): the oldest `group`
  * residual tokens k_blk/v_blk [group][d] are quantized (keys channel-wise,
  * values optionally post-rotated then token-wise) and, when w1k != NULL, the

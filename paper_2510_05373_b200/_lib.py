@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import POINTER, c_int, c_int32, c_int64, c_size_t, c_void_p
+from ctypes import c_double, POINTER, c_int, c_int32, c_int64, c_size_t, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("KVLC_LIB") or os.path.join(_HERE, "libkvlinc.so")  # KVLC_LIB: tracing build
@@ -50,6 +50,12 @@ _SIGS = {
     "kvlc_last_error": (ctypes.c_char_p, []),
     "kvlc_device_ok": (c_int, []),
     "kvlc_note_cache_write": (None, [POINTER(KvlcCache)]),
+    "kvlc_adapter_grads_workspace": (c_size_t, [c_int64, c_int, c_int, c_int]),
+    "kvlc_adapter_grads": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int,
+                                   c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "kvlc_adam_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_double, c_double, c_double,
+                               c_double, c_int64, c_void_p]),
     "kvlc_corrected_attention_workspace": (c_size_t, [c_int64, c_int, c_int]),
     "kvlc_corrected_attention": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int, c_int,
                                          c_void_p, c_void_p, c_size_t, c_void_p]),
