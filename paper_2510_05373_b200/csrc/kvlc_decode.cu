@@ -287,43 +287,78 @@ __device__ __forceinline__ void run_corr_unit(const DecArgs& a, int unit, float*
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   const size_t qh0 = (size_t)b * c.Hq + (size_t)kvh * NG;
+  constexpr int PART = WARPS * 2 * NG * HALF;          // per-warp partial z of both halves
+  constexpr int REG = PART > NG * RANK ? PART : NG * RANK;
   float* qs = smf;                    // [NG][D]
-  float* phs = qs + NG * D;           // [NG][RANK]
-  float* red = phs + NG * RANK;       // [WARPS][2 NG]
+  float* part = qs + NG * D;          // [WARPS][2][NG][HALF], then phs [NG][RANK] (aliased)
+  float* phs = part;
+  float* red = part + REG;            // [WARPS][2 NG]
   float* stat = red + WARPS * 2 * NG; // [2 NG]
-  griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
-  for (int i = t; i < NG * D; i += THREADS) qs[i] = bf2f(a.q[(qh0 + i / D) * D + i % D]);
-  __syncthreads();
-  float z[2][NG];
+  // the unit's S rows into L2 (row t, 1 KB) while phi_q is computed (r02, as run_corr)
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 1024;\n" ::"l"(c.S + ((size_t)unit * D + t) * RANK)
+               : "memory");
+  // z = q W_h for both halves: warp w takes channels 32w..32w+31, lane l features 4l..4l+3
+  // (16-B loads of W rows, 16 in flight), the warps' partial sums meet in shared memory
+  constexpr int PB = 16;
+  float4 w[PB];
+  const float4* const W1 = reinterpret_cast<const float4*>(a.w1q + ((size_t)kvh * D + 32 * warp) * HALF) + lane;
+  const float4* const W2 = reinterpret_cast<const float4*>(a.w2q + ((size_t)kvh * D + 32 * warp) * HALF) + lane;
 #pragma unroll
-  for (int i = 0; i < NG; ++i) z[0][i] = z[1][i] = 0.f;
-  const float* W1 = a.w1q + (size_t)kvh * D * HALF + t;
-  const float* W2 = a.w2q + (size_t)kvh * D * HALF + t;
-  constexpr int PB = 8;  // channels per batch of W1 + W2 loads in flight (16 / 32 measured slower)
-#pragma unroll 1
-  for (int c0 = 0; c0 < D; c0 += PB) {
-    float w1[PB], w2[PB];
+  for (int k = 0; k < PB; ++k) w[k] = __ldg(W1 + k * (HALF / 4));   // L2-resident: before the wait
+  griddep_wait();  // q may come from a programmatic-launch predecessor (kvlc_stage_input)
+  {  // all NG loads in flight before the shared-memory stores
+    uint16_t qv[NG];
+#pragma unroll
+    for (int i = 0; i < NG; ++i) qv[i] = __ldg(a.q + (qh0 + i) * D + t);
+#pragma unroll
+    for (int i = 0; i < NG; ++i) qs[i * D + t] = bf2f(qv[i]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {  // (half, channel slice) rounds of PB rows
+    const int hh = r >> 1, c0 = 32 * warp + PB * (r & 1);
+    float zz[NG][4];
+#pragma unroll
+    for (int i = 0; i < NG; ++i) zz[i][0] = zz[i][1] = zz[i][2] = zz[i][3] = 0.f;
 #pragma unroll
     for (int k = 0; k < PB; ++k) {
-      w1[k] = __ldg(W1 + (size_t)(c0 + k) * HALF);
-      w2[k] = __ldg(W2 + (size_t)(c0 + k) * HALF);
-    }
-#pragma unroll
-    for (int k = 0; k < PB; k += 4) {
 #pragma unroll
       for (int i = 0; i < NG; ++i) {
-        const float4 x = *reinterpret_cast<const float4*>(qs + i * D + c0 + k);
-        z[0][i] = fmaf(x.x, w1[k], z[0][i]);
-        z[0][i] = fmaf(x.y, w1[k + 1], z[0][i]);
-        z[0][i] = fmaf(x.z, w1[k + 2], z[0][i]);
-        z[0][i] = fmaf(x.w, w1[k + 3], z[0][i]);
-        z[1][i] = fmaf(x.x, w2[k], z[1][i]);
-        z[1][i] = fmaf(x.y, w2[k + 1], z[1][i]);
-        z[1][i] = fmaf(x.z, w2[k + 2], z[1][i]);
-        z[1][i] = fmaf(x.w, w2[k + 3], z[1][i]);
+        const float x = qs[i * D + c0 + k];
+        zz[i][0] = fmaf(x, w[k].x, zz[i][0]);
+        zz[i][1] = fmaf(x, w[k].y, zz[i][1]);
+        zz[i][2] = fmaf(x, w[k].z, zz[i][2]);
+        zz[i][3] = fmaf(x, w[k].w, zz[i][3]);
+      }
+    }
+    if (r + 1 < 4) {
+      const int h2 = (r + 1) >> 1, o2 = PB * ((r + 1) & 1);
+#pragma unroll
+      for (int k = 0; k < PB; ++k) w[k] = __ldg((h2 ? W2 : W1) + (o2 + k) * (HALF / 4));
+    }
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      float4* dst = reinterpret_cast<float4*>(part + ((warp * 2 + hh) * NG + i) * HALF + 4 * lane);
+      if (r & 1) {
+        float4 o = *dst;
+        o.x += zz[i][0]; o.y += zz[i][1]; o.z += zz[i][2]; o.w += zz[i][3];
+        *dst = o;
+      } else {
+        *dst = make_float4(zz[i][0], zz[i][1], zz[i][2], zz[i][3]);
       }
     }
   }
+  __syncthreads();
+  float z[2][NG];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < NG; ++i) {
+      float v = part[(h * NG + i) * HALF + t];
+#pragma unroll
+      for (int w2 = 1; w2 < WARPS; ++w2) v += part[((w2 * 2 + h) * NG + i) * HALF + t];
+      z[h][i] = v;
+    }
   // max-shifted softmax of each half (linalg.py:38-47)
 #pragma unroll
   for (int h = 0; h < 2; ++h)
@@ -1268,10 +1303,16 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   }();
   // Measured (r02, same box): one-wave grids gain (config 3 B1 x 4k 16.0 -> 13.3 us, B16 x 4k
   // 24.9 -> 21.3), multi-wave grids lose (config 2 36.8 -> 38.6, config 3 B16 x 8k 26.4 -> 31.0:
-  // the long tail tasks hold slots the splits need), so fused only when everything fits one wave
+  // the long tail tasks hold slots the splits need), so fused only when everything fits one wave.
+  // And only for groups of more than 4 heads: after the correction unit's phi loads were
+  // batched, one-wave grids of small groups run faster with a whole-unit correction CTA beside
+  // two residual CTAs (B1 x 4k, 8 kv heads: NG 1 9.29 -> 8.59 us, NG 2 9.43 -> 9.26, NG 4
+  // 10.29 -> 10.49, NG 4 at 32k 15.55 -> 14.65, NG 8 13.36 -> 16.43; Qwen NG 7 keeps fusing:
+  // B1 x 32k 13.9 vs 15.3).  KVLC_TAILFUSE=0 off, 1 auto, 2 any group size.
   const bool one_wave = (long long)p.U * (p.nsq + 2) <= 148LL * split_minb(NG);
-  if (tail && p.corr_on && tailfuse_env && one_wave && !corr_split_env) a.corr_split = 2;
-  a.tail_fused = tail && p.corr_on && a.corr_split == 2 && tailfuse_env && one_wave;
+  const bool fuse = tailfuse_env == 2 || (tailfuse_env == 1 && NG > 4);
+  if (tail && p.corr_on && fuse && one_wave && !corr_split_env) a.corr_split = 2;
+  a.tail_fused = tail && p.corr_on && a.corr_split == 2 && fuse && one_wave;
   int grid = p.U * p.nsq + (tail ? (a.tail_fused ? 0 : 2 * p.U) + (p.corr_on ? a.corr_split * p.U : 0) : 0);
   // persistent split grid (warp-per-chunk kernel, separate combine): at most one wave of
   // CTAs that take tasks from a counter.  Measured slower (config 2 split 37.0 -> 38.1 us

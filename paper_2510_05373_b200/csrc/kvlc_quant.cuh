@@ -154,6 +154,7 @@ __device__ __forceinline__ void qb_wait(uint64_t* bar, uint32_t parity) {
 union SplitSmem {
   QuantSmem quant;
   float rec[WARPS * 8 * REC];
+  float corr[8 * D + WARPS * 2 * 8 * HALF + WARPS * 2 * 8 + 2 * 8];  // run_corr_unit, NG <= 8
 };
 
 // Thread 0: chunk cb (absolute) into stage `st`, completion on `bar`.
