@@ -707,11 +707,45 @@ __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE],
 // packed words, fp16 metadata into the cache; fp32 scale / zero and the value
 // codes (bytes) into a scratch the tensor-core state kernel reconstructs k_err
 // and v_q from (cache.py:141-154).
+constexpr int VT_LD = D + 2;  // staged ring values: row stride (2-way store conflicts at most)
 struct QkSmem {
   uint8_t codes[G * D];  // value codes [token][channel] (swizzled, vsw)
   double2 kpar[D];
   float4 kparf[D];
+  uint16_t vt[G / 2][VT_LD];  // a value CTA's ring tokens, token-major (vsplit >= 2)
+  double dv[FT_THREADS / 32][D];  // per warp: the token of a dense re-evaluation, fp64
 };
+#ifdef KVLC_TRACE
+__device__ long long g_qtrace[16][128][4];  // quant CTA (0, unit, z): globaltimer start, K1 done, end; SM id
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define QT_STAMP(i)                                                                              \
+  do {                                                                                           \
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.z < 16 && blockIdx.y < 128) {            \
+      g_qtrace[blockIdx.z][blockIdx.y][i] = gtimer();                                            \
+      if (i == 0) {                                                                              \
+        unsigned smid;                                                                           \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                                        \
+        g_qtrace[blockIdx.z][blockIdx.y][3] = smid;                                              \
+      }                                                                                          \
+    }                                                                                            \
+  } while (0)
+// V CTA z = 1, warp 0: per token iteration end time and the fallback level taken (0 fast, 1 fp64 FWHT, 2 dense)
+__device__ long long g_qtok[128][24][2];
+#define QT_TOK(ti, lvl)                                                                           \
+  do {                                                                                            \
+    if (lane == 0 && warp == 0 && blockIdx.x == 0 && blockIdx.z == 1 && blockIdx.y < 128 && (ti) < 24) { \
+      g_qtok[blockIdx.y][ti][0] = gtimer();                                                       \
+      g_qtok[blockIdx.y][ti][1] = (lvl);                                                          \
+    }                                                                                             \
+  } while (0)
+#else
+#define QT_STAMP(i) do {} while (0)
+#define QT_TOK(ti, lvl) do {} while (0)
+#endif
 #ifndef KVLC_QK_MINB
 #define KVLC_QK_MINB 3  // 3 CTAs per SM (80 registers, 84 B spills) measured 2 % faster than 2
 #endif
@@ -723,6 +757,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
   if (ci >= seq.nflush[b]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool writer = true;
+  QT_STAMP(0);
   // prefill: chunk ci of the sequence's tokens; ring (decode-time flush): the oldest G slots of
   // the residual ring into the sequence's next chunk (cache.py:132-147)
   const int64_t tok0 = a.ring ? (int64_t)c.res_start[b] + (int64_t)ci * G : (int64_t)ci * G;
@@ -796,6 +831,10 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       __syncwarp();
       uint32_t cw[4] = {0u, 0u, 0u, 0u};  // K words t0 = 0..3 of this lane's tokens
       uint8_t* aimg = a.aimg + slot * 2 * FT_TILE;
+      // elements near a rounding tie (bit 4e + r) are re-decided after the loop: an inlined
+      // fp64 division per element made the unrolled loop ~60 KB of SASS (instruction-fetch
+      // stalls, the key CTA of a ring flush took ~35 us)
+      uint64_t tie = 0;
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const float4 pf = sm.kparf[ch0 + e];
@@ -807,12 +846,8 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
           if (scf > 0.f) {
             const float q = (x[r][e] - mnf) * invf;
             const float fr = q - floorf(q);
-            if (fabsf(fr - 0.5f) < 1e-5f) {  // near a tie: the exact fp64 decision
-              const double2 pr = sm.kpar[ch0 + e];
-              code = code_of((double)x[r][e], pr.x, pr.y, 3);
-            } else {
-              code = (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f);
-            }
+            tie |= (uint64_t)(fabsf(fr - 0.5f) < 1e-5f) << (4 * e + r);
+            code = (uint32_t)fminf(fmaxf(rintf(q), 0.f), 3.f);
           }
           // byte q of word t0 holds channel 16kt + 2t0 + {0,8,1,9}[q]; bit pair r holds token 4l + r
           const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
@@ -825,6 +860,24 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         *reinterpret_cast<uint2*>(aimg + off) = *reinterpret_cast<const uint2*>(ehi);
         *reinterpret_cast<uint2*>(aimg + FT_TILE + off) = *reinterpret_cast<const uint2*>(elo);
       }
+      while (tie) {  // the exact fp64 decision (quantize.py:202-207) for the near-tie elements
+        const int bit = __ffsll((long long)tie) - 1;
+        tie &= tie - 1;
+        const int e = bit >> 2, r = bit & 3;
+        const float xv = bf2f(K[(size_t)(4 * lane + r) * D + ch0 + e]);
+        const double2 pr = sm.kpar[ch0 + e];
+        const uint32_t code = code_of((double)xv, pr.x, pr.y, 3);
+        const int t0 = (e & 7) >> 1, sh = 8 * (((e & 1) << 1) | (e >> 3)) + 2 * r;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k == t0) cw[k] = (cw[k] & ~(3u << sh)) | (code << sh);
+        const float4 pf = sm.kparf[ch0 + e];
+        __half hi, lo;
+        ft_hilo(xv - fmaf((float)code, pf.y, pf.x), hi, lo);
+        const int off = ft_off_a(4 * lane, ch0 + e) + 2 * r;
+        *reinterpret_cast<__half*>(aimg + off) = hi;
+        *reinterpret_cast<__half*>(aimg + FT_TILE + off) = lo;
+      }
       if (writer) {
         const int wt = lane >> 3, g = lane & 7;  // tokens 32 wt + 4 g + r
 #pragma unroll
@@ -832,10 +885,36 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       }
     }
   }
+  QT_STAMP(1);
   // token range of K2: the whole chunk, or 32-token slice zpart - 1
   const int t_lo = a.vsplit ? (zpart - 1) * (G / a.vsplit) : 0;
   const int ntok_w = a.vsplit ? G / a.vsplit / (FT_THREADS / 32) : G / (FT_THREADS / 32);  // per warp
   if (a.vsplit == 0 || zpart > 0) {
+    // The ring holds values channel-major ([D][SLOTS], for the decode's residual MMAs): a
+    // value CTA of <= 64 tokens stages its slice token-major in shared memory with 16-B loads
+    // along the slot axis (per-lane 2-B gathers from 128 channel rows made the value CTAs of a
+    // decode-time flush take ~20 us)
+    const int ntok = a.vsplit ? G / a.vsplit : G;
+    const bool staged = a.v_c != 1 && a.v_t == 1 && ntok <= G / 2 && ntok % 8 == 0 &&
+                        (reinterpret_cast<uintptr_t>(V) & 15) == 0 && (a.v_c & 7) == 0;
+    if (staged) {
+      const int per_row = ntok / 8;
+      for (int i = tid; i < D * per_row; i += FT_THREADS) {
+        const int ch = i / per_row, tg = i % per_row;
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(V + (size_t)ch * a.v_c + t_lo + 8 * tg));
+        const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sm.vt[8 * tg + j][ch] = (uint16_t)(wv[j >> 1] >> (16 * (j & 1)));
+      }
+      __syncthreads();
+    }
+    auto ldv2 = [&](int t) -> uint2 {
+      if (staged) {
+        const uint32_t* p = reinterpret_cast<const uint32_t*>(&sm.vt[t - t_lo][lane * 4]);
+        return make_uint2(p[0], p[1]);
+      }
+      return ldv(t);
+    };
     // ---- K2: values, FWHT post-rotation (fp32, guarded), token-wise quantization ----
     // The fp32 FWHT differs from the reference's fp64 dense x @ H in the last bits:
     // a token whose quotient lies near a rounding tie or whose scale / zero lies near
@@ -845,17 +924,29 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
     uint2 vpf[VPF];
 #pragma unroll
     for (int i = 0; i < VPF; ++i)
-      if (i < ntok_w) vpf[i] = ldv(t_lo + warp + 8 * i);
+      if (!staged && i < ntok_w) vpf[i] = ldv(t_lo + warp + 8 * i);
+    QT_TOK(0, 0);
+#ifdef KVLC_TRACE
+    int n_lvl = 0;
+#endif
 #pragma unroll 1
     for (int ti = 0; ti < ntok_w; ++ti) {
       const int t = t_lo + warp + 8 * ti;
+      int lvl = 0;
+#ifdef KVLC_TRACE
+      if (ti == 0) n_lvl = 0;
+#endif
       float xf[4];
       {
-        uint2 raw = vpf[0];
+        uint2 raw;
+        if (staged) {
+          raw = ldv2(t);
+        } else {
+          raw = vpf[0];
 #pragma unroll
-        for (int i = 0; i < VPF - 1; ++i) vpf[i] = vpf[i + 1];
-        if (ti + VPF < ntok_w)
-          vpf[VPF - 1] = ldv(t + 8 * VPF);
+          for (int i = 0; i < VPF - 1; ++i) vpf[i] = vpf[i + 1];
+          if (ti + VPF < ntok_w) vpf[VPF - 1] = ldv(t + 8 * VPF);
+        }
         xf[0] = __uint_as_float(raw.x << 16);
         xf[1] = __uint_as_float(raw.x & 0xffff0000u);
         xf[2] = __uint_as_float(raw.y << 16);
@@ -892,13 +983,15 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       // rounding tie or its zero / scale lies near an fp16 rounding midpoint (the stored
       // metadata is float16 of the reference's fp64 value, cache.py:220-224).
       const float range = mxf - mnf;
-      const float scf = range * (1.f / 3.f), invf = range > 0.f ? 3.f / range : 0.f;
+      // approximate divisions: invf feeds only the fast-path quotients (error ~1e-7, inside
+      // qtol) and the rest are tolerances
+      const float scf = range * (1.f / 3.f), invf = range > 0.f ? __fdividef(3.f, range) : 0.f;
       const float ferr = 4e-6f * fmaxf(fabsf(mnf), fabsf(mxf));
       auto near_mid = [](float v, float rel) {
         return __half_as_ushort(__float2half_rn(v * (1.f - rel))) != __half_as_ushort(__float2half_rn(v * (1.f + rel)));
       };
-      bool amb = near_mid(mnf, ferr / fmaxf(fabsf(mnf), 1e-30f) + 2e-7f) ||
-                 (range > 0.f && near_mid(scf, 2.f * ferr / range + 2e-7f));
+      bool amb = near_mid(mnf, __fdividef(ferr, fmaxf(fabsf(mnf), 1e-30f)) + 2e-7f) ||
+                 (range > 0.f && near_mid(scf, __fdividef(2.f * ferr, range) + 2e-7f));
       const float qtol = 1e-4f + 4.f * ferr * invf;
       uint32_t code[4];
 #pragma unroll
@@ -916,12 +1009,16 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       float vsc = (float)(((double)mxu - (double)mnu) * (hsd / 3.0));
       float vmid = (float)(0.5 * ((double)mnu + (double)mxu) * hsd);
       uint16_t meta_s = __half_as_ushort(__float2half_rn(scf)), meta_z = __half_as_ushort(__float2half_rn(mnf));
+#ifdef KVLC_FORCE_DENSE
+      amb = true;
+#endif
       if (__any_sync(0xffffffffu, amb)) {
+        lvl = 1;
         // fp64 FWHT: agrees with the dense fp64 x @ H to an ulp
         const double hs = 1.0 / sqrt((double)D);
         double x[4], y[4];
         {
-          const uint2 raw = ldv(t);
+          const uint2 raw = ldv2(t);
           y[0] = (double)__uint_as_float(raw.x << 16);
           y[1] = (double)__uint_as_float(raw.x & 0xffff0000u);
           y[2] = (double)__uint_as_float(raw.y << 16);
@@ -957,20 +1054,40 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
           const double r = __dsub_rn(x[e], mn) * inv;
           amb2 |= scale > 0.0 && fabs(r - floor(r) - 0.5) < 1e-9;
         }
+#ifdef KVLC_FORCE_DENSE  // timing probe: every ambiguous token takes the dense path
+        amb2 = true;
+#endif
         if (__any_sync(0xffffffffu, amb2)) {  // a genuine tie: the reference's dense x @ H order
+          lvl = 2;
           mn = INFINITY;
           mx = -INFINITY;
+          // the lane's 4 channel chains interleaved (each chain keeps its j order: the same
+          // sums as one chain after another, ~4x less latency; the serial form cost ~19 us)
+          // H[j][4 lane + e] = (-1)^(popc(J & lane) + popc(r & e)) hs for j = 4 J + r
+          {
+            const uint2 rw = ldv2(t);  // the token in fp64 in shared memory (one conversion per value)
+            double4* d4 = reinterpret_cast<double4*>(&sm.dv[warp][4 * lane]);
+            *d4 = make_double4((double)__uint_as_float(rw.x << 16), (double)__uint_as_float(rw.x & 0xffff0000u),
+                               (double)__uint_as_float(rw.y << 16), (double)__uint_as_float(rw.y & 0xffff0000u));
+            __syncwarp();
+          }
+          double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+          for (int J = 0; J < D / 4; ++J) {
+            const double sg = (__popc((unsigned)(J & lane)) & 1) ? -hs : hs;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              const double v = sm.dv[warp][4 * J + r];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[e] = fma(v, (__popc(r & e) & 1) ? -sg : sg, acc[e]);
+            }
+          }
+          __syncwarp();
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int ch = lane * 4 + e;
-            double acc = 0.0;
-            for (int j = 0; j < D; ++j) {
-              const double hj = (__popc((unsigned)(j & ch)) & 1) ? -hs : hs;
-              acc = fma((double)bf2f(V[t * a.v_t + j * a.v_c]), hj, acc);
-            }
-            x[e] = acc;
-            mn = fmin(mn, acc);
-            mx = fmax(mx, acc);
+            x[e] = acc[e];
+            mn = fmin(mn, acc[e]);
+            mx = fmax(mx, acc[e]);
           }
           mn = warp_min_d(mn);
           mx = warp_max_d(mx);
@@ -992,8 +1109,8 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
          // (z alone is ~ -2 for N(0,1) rows, S ~ 0.5), the per-token power of two 2^e puts
          // s 2^e in [2^10, 2^11) so the fp16 hi / lo split of s 2^e Phi stays out of the
          // subnormal range, and (code - 3/2) 2^-e is exact in fp16
-        int ex;
-        frexpf(vsc > 0.f ? vsc : 1.f, &ex);
+        // frexpf exponent from the bits (a subnormal vsc clamps to e = 22 either way)
+        const int ex = (int)((__float_as_uint(vsc > 0.f ? vsc : 1.f) >> 23) & 0xffu) - 126;
         const int e = min(max(11 - ex, -14), 22);
         const float cs = __int_as_float((127 - e) << 23);  // 2^-e
         auto hc = [&](uint32_t cd) { return (uint32_t)__half_as_ushort(__float2half_rn(((float)cd - 1.5f) * cs)); };
@@ -1005,12 +1122,29 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         c.vscale[cb * G + t] = meta_s;
         c.vzero[cb * G + t] = meta_z;
       }
+      QT_TOK(ti + 1, lvl);
+#ifdef KVLC_TRACE
+      n_lvl += lvl == 1 ? 1 : lvl == 2 ? 256 : 0;
+#endif
     }
+#ifdef KVLC_TRACE
+    if (lane == 0 && blockIdx.x == 0 && blockIdx.z == 1 && blockIdx.y < 128) {
+      g_qtok[blockIdx.y][9 + warp][0] = gtimer();
+      g_qtok[blockIdx.y][9 + warp][1] = n_lvl;
+    }
+#endif
     __syncthreads();
+#ifdef KVLC_TRACE
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.z == 1 && blockIdx.y < 128) g_qtok[blockIdx.y][17][0] = gtimer();
+#endif
     // V words of the CTA's slices (a word covers tokens of one 32-token slice: 256 words each)
     const int w_lo = a.vsplit ? (zpart - 1) * (1024 / a.vsplit) : 0, w_hi = a.vsplit ? w_lo + 1024 / a.vsplit : 1024;
     for (int wi = w_lo + tid; wi < w_hi; wi += FT_THREADS) c.vcodes[cb * 1024 + wi] = frag_store(pack_v_word_sw(sm.codes, wi));
   }
+  QT_STAMP(2);
+#ifdef KVLC_TRACE
+  if (tid == 0 && blockIdx.x == 0 && blockIdx.z == 1 && blockIdx.y < 128) g_qtok[blockIdx.y][18][0] = gtimer();
+#endif
 }
 
 #ifdef KVLC_TRACE
@@ -1286,6 +1420,12 @@ __global__ void prep_wtiles_kernel(kvlc_adapter ad, int Hkv, uint8_t* __restrict
 
 #ifdef KVLC_TRACE
 }  // namespace
+int kvlc_qtok_copy(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, g_qtok, bytes < sizeof(g_qtok) ? bytes : sizeof(g_qtok)) == cudaSuccess ? 0 : 2;
+}
+int kvlc_qtrace_copy(void* dst, size_t bytes) {
+  return cudaMemcpyFromSymbol(dst, g_qtrace, bytes < sizeof(g_qtrace) ? bytes : sizeof(g_qtrace)) == cudaSuccess ? 0 : 2;
+}
 int kvlc_ftrace_copy(void* dst, size_t bytes) {
   return cudaMemcpyFromSymbol(dst, g_ftrace, bytes < sizeof(g_ftrace) ? bytes : sizeof(g_ftrace)) == cudaSuccess ? 0 : 2;
 }
