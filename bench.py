@@ -356,22 +356,25 @@ def run_serving_loop(cache, q, bank, dev):
         step.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(n - 3):
         step.replay()
     e1.record()
+    step.replay()                            # every sequence flushes one chunk
+    e2.record()
     torch.cuda.synchronize()
     step_us = e0.elapsed_time(e1) * 1e3 / (n - 3)
-    e0.record()
-    step.replay()                            # every sequence flushes one chunk
-    e1.record()
-    torch.cuda.synchronize()
-    flush_us = e0.elapsed_time(e1) * 1e3
+    # queued behind the steady steps like every other step of the loop (its graph launch
+    # overlaps the GPU work ahead of it; r02 before: timed from an idle GPU, ~20 us of
+    # host graph-launch latency inside)
+    flush_us = e1.elapsed_time(e2) * 1e3
     return {"graph_step_us": step_us, "flush_step_us": flush_us,
             "us_per_step_amortised": (127 * step_us + flush_us) / 128,
             "note": "append + decode per step, one CUDA graph launch each (steady state, second flush "
                     "period); the flushing step (all 128 units in lockstep) is a graph with the tensor-core "
-                    "ring flush (quant_kernel split over 5 CTAs per unit, flush_tc_kernel adding into S)"}
+                    "ring flush (quant_kernel: a key CTA + 2 value CTAs per unit, flush_tc_kernel adding "
+                    "into S), timed queued behind the steady steps like them"}
 
 
 def run_other_configs(dev, peak_gbs):

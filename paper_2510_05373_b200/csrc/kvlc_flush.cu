@@ -133,6 +133,11 @@ struct FlushArgs {
   // 0 = one CTA per chunk does K1 and K2; n > 0 = blockIdx.z 0 does K1, z = 1..n do K2 on
   // the tokens of 32-token slice z - 1 (n = G / 32)
   int vsplit;
+  // the phi GEMM W tiles, prepared by quant_kernel's first CTAs (no separate launch)
+  uint8_t* wtiles;
+  int prep_n;                // 16 * Hkv * 2 blocks of 256 threads, 0 = none
+  int finalize;              // flush_tc_kernel CTA 0 applies append_finalize (ring flushes)
+  int both;                  // flush_tc_kernel: one CTA per unit runs both feature halves (one chunk)
 };
 
 __global__ void __launch_bounds__(FLUSH_THREADS, 1) flush_kernel(const FlushArgs a, const SeqInfo seq) {
@@ -423,7 +428,8 @@ __global__ void append_kernel(kvlc_cache c, const uint16_t* __restrict__ k_t,
   c.vres[((size_t)unit * D + ch) * SLOTS + slot] = v_t[(size_t)unit * D + ch];
 }
 
-__global__ void append_finalize_kernel(kvlc_cache c, const SeqInfo seq) {
+// ring counters after an append (+ flush of the due sequences): cache.py:120-147
+__device__ __forceinline__ void append_finalize(const kvlc_cache& c, const SeqInfo& seq) {
   for (int b = threadIdx.x; b < c.B; b += blockDim.x) {
     int len = c.res_len[b] + (seq.is_active(b) ? 1 : 0);
     if (seq.is_flush(b)) {
@@ -434,6 +440,7 @@ __global__ void append_finalize_kernel(kvlc_cache c, const SeqInfo seq) {
     c.res_len[b] = len;
   }
 }
+__global__ void append_finalize_kernel(kvlc_cache c, const SeqInfo seq) { append_finalize(c, seq); }
 
 __global__ void export_chunk_kernel(kvlc_cache c, int unit, int chunk, uint32_t* kw, uint32_t* vw,
                                     uint16_t* ks, uint16_t* kz, uint16_t* vs, uint16_t* vz) {
@@ -615,7 +622,7 @@ __global__ void deserialize_unit_kernel(kvlc_cache c, int unit, int n, int n_res
 //       end.  The next chunk's A_phi image streams in while the softmax and S GEMM run.
 constexpr int FT_THREADS = 256;
 constexpr int FT_TILE = 32768;              // [128][128] fp16 tile
-constexpr uint32_t FT_COL_PHI = 0, FT_COL_S = 128, FT_TMEM = 256;
+constexpr uint32_t FT_COL_PHI = 0, FT_COL_S = 128, FT_TMEM = 256, FT_TMEM2 = 512;  // 2: S of both halves
 constexpr uint32_t FT_IDESC_PHI = (1u << 4) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | (8u << 24);
 
 struct FtSmem {
@@ -707,6 +714,20 @@ __device__ __forceinline__ void ft_gemm(uint32_t d, const uint8_t (*a)[FT_TILE],
 // packed words, fp16 metadata into the cache; fp32 scale / zero and the value
 // codes (bytes) into a scratch the tensor-core state kernel reconstructs k_err
 // and v_q from (cache.py:141-154).
+// W1k / W2k (fp32 [Hkv][128][128]) -> fp16 hi / lo B tiles of the phi GEMM,
+// [kvh][half][hi, lo][FT_TILE]: element (k = channel, n = feature); block x of 16 per (kvh, h).
+__device__ __forceinline__ void prep_wtiles_block(const kvlc_adapter& ad, int x, int kvh, int h, uint8_t* out) {
+  const float* W = (h == 0 ? ad.w1k : ad.w2k) + (size_t)kvh * D * HALF;
+  uint8_t* hi = out + ((size_t)kvh * 2 + h) * 2 * FT_TILE;
+  uint8_t* lo = hi + FT_TILE;
+  for (int i = x * 256 + (int)threadIdx.x; i < D * HALF; i += 16 * 256) {
+    const int ch = i / HALF, f = i % HALF;
+    __half xh, yl;
+    ft_hilo(__ldg(W + i), xh, yl);
+    *reinterpret_cast<__half*>(hi + ft_off(f, ch)) = xh;
+    *reinterpret_cast<__half*>(lo + ft_off(f, ch)) = yl;
+  }
+}
 constexpr int VT_LD = D + 2;  // staged ring values: row stride (2-way store conflicts at most)
 struct QkSmem {
   uint8_t codes[G * D];  // value codes [token][channel] (swizzled, vsw)
@@ -754,6 +775,11 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
   const kvlc_cache& c = a.c;
   const int unit = blockIdx.y, ci = blockIdx.x;
   const int b = unit / c.Hkv;
+  if (a.prep_n) {  // the state kernel's W tiles (16 blocks per (kvh, half)) over the first CTAs
+    const int lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int nblk = gridDim.x * gridDim.y * gridDim.z;
+    for (int p = lin; p < a.prep_n; p += nblk) prep_wtiles_block(a.ad, p % 16, (p / 16) % c.Hkv, p / (16 * c.Hkv), a.wtiles);
+  }
   if (ci >= seq.nflush[b]) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool writer = true;
@@ -932,8 +958,8 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
 #pragma unroll 1
     for (int ti = 0; ti < ntok_w; ++ti) {
       const int t = t_lo + warp + 8 * ti;
-      int lvl = 0;
 #ifdef KVLC_TRACE
+      int lvl = 0;
       if (ti == 0) n_lvl = 0;
 #endif
       float xf[4];
@@ -1013,7 +1039,9 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       amb = true;
 #endif
       if (__any_sync(0xffffffffu, amb)) {
+#ifdef KVLC_TRACE
         lvl = 1;
+#endif
         // fp64 FWHT: agrees with the dense fp64 x @ H to an ulp
         const double hs = 1.0 / sqrt((double)D);
         double x[4], y[4];
@@ -1058,7 +1086,9 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
         amb2 = true;
 #endif
         if (__any_sync(0xffffffffu, amb2)) {  // a genuine tie: the reference's dense x @ H order
+#ifdef KVLC_TRACE
           lvl = 2;
+#endif
           mn = INFINITY;
           mx = -INFINITY;
           // the lane's 4 channel chains interleaved (each chain keeps its j order: the same
@@ -1151,12 +1181,16 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
 __device__ long long g_ftrace[2][40][10];  // CTA (0, 0, h): per chunk clock64 at phase boundaries (thread 0)
 #define FT_STAMP(i)                                                                            \
   do {                                                                                         \
-    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && it < 40) g_ftrace[h][it][i] = clock64(); \
+    if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0 && it < 40) g_ftrace[h0 + hp][it][i] = clock64(); \
   } while (0)
-// kernel phases of CTA (0, 0, h) in slot 39: entry, setup done, chunk loop done, drain done
+// kernel phases of CTA (0, 0, h0) in slot 39: entry, setup done, chunk loop done, drain done
 #define FT_PHASE(i) \
-  do { if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_ftrace[h][39][i] = clock64(); } while (0)
+  do { if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_ftrace[h0][39][i] = clock64(); } while (0)
+// drain steps of pass hp in slot 38: start, P done, tile written, rows written
+#define FT_DRAIN(i) \
+  do { if (tid == 0 && blockIdx.x == 0 && blockIdx.y == 0) g_ftrace[h0 + hp][38][i] = clock64(); } while (0)
 #else
+#define FT_DRAIN(i) do { } while (0)
 #define FT_STAMP(i) \
   do {              \
   } while (0)
@@ -1201,23 +1235,34 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   extern __shared__ __align__(1024) uint8_t ft_raw[];
   FtSmem& sm = *reinterpret_cast<FtSmem*>(ft_raw);
   const kvlc_cache& c = a.c;
-  const int unit = blockIdx.y, split = blockIdx.x, h = blockIdx.z;
+  const int unit = blockIdx.y, split = blockIdx.x;
+  // feature halves of this CTA: blockIdx.z, or both in turn (a.both: one chunk per CTA, the
+  // decode-time ring flush; 128 CTAs in one wave instead of 256 in two)
+  const int h0 = a.both ? 0 : (int)blockIdx.z, npass = a.both ? 2 : 1;
   const int b = unit / c.Hkv, kvh = unit % c.Hkv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nf = seq.nflush[b];
   const int c_lo = split * a.cpc, c_hi = min(nf, c_lo + a.cpc);
+  if (a.finalize && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) append_finalize(c, seq);
   if (c_lo >= c_hi) return;
   const size_t slot0 = (size_t)unit * a.slot_stride;
   FT_PHASE(0);
+  if (!a.s_out && tid <= D) {  // the drain's read-modify-write rows (S, P: this CTA's halves) into L2 now
+    const float* row = (tid < D ? c.S + ((size_t)unit * D + tid) * RANK : c.P + (size_t)unit * RANK) + h0 * HALF;
+    if (npass == 2)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 1024;\n" ::"l"(row) : "memory");
+    else
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], 512;\n" ::"l"(row) : "memory");
+  }
 
-  // resident W_h tiles (prepared by prep_wtiles_kernel), TMEM, barriers, first images
+  // resident W_h tiles (prepared by quant_kernel), TMEM, barriers, first images
   {
-    const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + h) * 2 * FT_TILE);
+    const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + h0) * 2 * FT_TILE);
     uint4* dst = reinterpret_cast<uint4*>(sm.w[0]);
     for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
     tc::cp_commit();
   }
-  if (warp == 0) tc::tmem_alloc(&sm.tbase, FT_TMEM);
+  if (warp == 0) tc::tmem_alloc(&sm.tbase, npass == 2 ? FT_TMEM2 : FT_TMEM);
   if (tid == 0) {
     tc::mbar_init(&sm.mphi, 1);
     tc::mbar_init(&sm.ms, 1);
@@ -1238,23 +1283,32 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   const int part = warp >> 2;
   // P[f] = sum_t phi[t][f], Z[f] = sum_t z_t phi[t][f] for this warp's 32 token rows:
   // lane owns features 64 part + 2 lane + {0, 1} (reduce-scatter order)
-  float pacc[2] = {0.f, 0.f}, zacc[2] = {0.f, 0.f};
+  float pacc[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, zacc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
   FT_PHASE(1);
+  if (npass == 2 && c_hi - c_lo != 1) __trap();  // both halves: the A / code tiles stay resident
 
-  for (int ci = c_lo; ci < c_hi; ++ci) {
-    const int it = ci - c_lo;
+  for (int pi = 0; pi < npass * (c_hi - c_lo); ++pi) {
+    // pass pi: chunk ci, half h0 + hp (both: pi = hp over the one chunk; else pi = it)
+    const int hp = npass == 2 ? pi : 0, ci = c_lo + (npass == 2 ? 0 : pi), it = pi;
     FT_STAMP(0);
     if (warp == 0) {  // phi GEMM: Z = k_err W_h (passes hi.hi, hi.lo once A hi has landed, lo.hi after A lo)
-      tc::mbar_wait(&sm.ma[0], (uint32_t)it & 1u);
+      if (hp == 0) tc::mbar_wait(&sm.ma[0], (uint32_t)it & 1u);
       tc::fence_after_sync();
-      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false, &sm.ma[1], (uint32_t)it & 1u, 2);
+      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false, hp == 0 ? &sm.ma[1] : nullptr,
+              (uint32_t)it & 1u, 2);
       tc::mma_commit_w(&sm.mphi);
     }
     FT_STAMP(1);
     tc::mbar_wait(&sm.mphi, (uint32_t)it & 1u);
     tc::fence_after_sync();
     if (tid == 0 && ci + 1 < c_hi) ft_load_a(sm, a, slot0 + ci + 1);  // A_phi consumed: next one in flight
-    tc::mbar_wait(&sm.mc, (uint32_t)it & 1u);  // this chunk's (s, z)
+    if (npass == 2 && hp == 0) {  // W of the second half into the freed W tiles (lands during the softmax)
+      const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + 1) * 2 * FT_TILE);
+      uint4* dst = reinterpret_cast<uint4*>(sm.w[0]);
+      for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
+      tc::cp_commit();
+    }
+    if (hp == 0) tc::mbar_wait(&sm.mc, (uint32_t)it & 1u);  // this chunk's (s, z)
     if (it > 0) tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);  // the previous S GEMM has read s' Phi
     FT_STAMP(2);
 
@@ -1316,18 +1370,19 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
           }
         }
       }
-      pacc[0] += z[0];
-      pacc[1] += z[1];
-      zacc[0] += w[0];
-      zacc[1] += w[1];
+      pacc[hp][0] += z[0];
+      pacc[hp][1] += z[1];
+      zacc[hp][0] += w[0];
+      zacc[hp][1] += w[1];
     }
+    if (npass == 2 && hp == 0) tc::cp_wait<0>();  // second half's W (before the barrier below)
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
     FT_STAMP(3);
     if (warp == 0) {  // S GEMM: D^T += codes^T (s' Phi), then the next code tile once it is read
       tc::fence_after_sync();
-      ft_gemm_s(tb + FT_COL_S, sm.cv, sm.ps[0], sm.ps[1], it > 0);
+      ft_gemm_s(tb + FT_COL_S + 128 * hp, sm.cv, sm.ps[0], sm.ps[1], npass == 1 && it > 0);
       tc::mma_commit_w(&sm.ms);
       if (ci + 1 < c_hi) {
         tc::mbar_wait(&sm.ms, (uint32_t)it & 1u);
@@ -1339,13 +1394,19 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   }
 
   // ---- drain: S[c][h*128 + f] = D^T[c][f] + (z^T Phi)[f] (cache.py:155-157), P[h*128 + f] ----
-  tc::mbar_wait(&sm.ms, (uint32_t)(c_hi - c_lo - 1) & 1u);
+  tc::mbar_wait(&sm.ms, (uint32_t)(npass * (c_hi - c_lo) - 1) & 1u);
   FT_PHASE(2);
   tc::fence_after_sync();
+#pragma unroll 1
+  for (int hp = 0; hp < npass; ++hp) {
+  const int h = h0 + hp;
+  if (hp > 0) __syncthreads();  // the previous half's tile / row reads are done
+  FT_DRAIN(0);
   float* zf = reinterpret_cast<float*>(sm.ps[0]);  // free now: [4 token groups][128 features][P, Z]
   {
     const int f = 64 * part + 2 * lane;
-    *reinterpret_cast<float4*>(zf + ((warp & 3) * 128 + f) * 2) = make_float4(pacc[0], zacc[0], pacc[1], zacc[1]);
+    *reinterpret_cast<float4*>(zf + ((warp & 3) * 128 + f) * 2) =
+        make_float4(pacc[hp][0], zacc[hp][0], pacc[hp][1], zacc[hp][1]);
   }
   __syncthreads();
   float* S = a.s_out ? a.s_out + ((size_t)unit * a.splits + split) * D * RANK : c.S + (size_t)unit * D * RANK;
@@ -1356,6 +1417,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     for (int g4 = 0; g4 < 4; ++g4) pf += zf[(g4 * 128 + tid) * 2];
     P[h * HALF + tid] += pf;
   }
+  FT_DRAIN(1);
   // S rows: TMEM -> a padded shared tile (the W / A tiles are free now) -> coalesced 16-B
   // read-modify-writes of whole S rows with the rank-1 term added (a thread per TMEM row
   // walking its row took ~20 us per CTA: every warp access touched 32 rows, r02
@@ -1370,7 +1432,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
 #pragma unroll 1
     for (int c0 = 64 * part; c0 < 64 * part + 64; c0 += 32) {
       float d[32];
-      tc::tmem_ld32(lane_addr + FT_COL_S + c0, reinterpret_cast<uint32_t*>(d));
+      tc::tmem_ld32(lane_addr + FT_COL_S + 128 * hp + c0, reinterpret_cast<uint32_t*>(d));
       tc::wait_ld();
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
@@ -1382,41 +1444,37 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
                (zf[(2 * 128 + f) * 2 + 1] + zf[(3 * 128 + f) * 2 + 1]);
     }
     __syncthreads();
-#pragma unroll  // all 16 row pieces of the thread in flight at once
-    for (int idx = tid; idx < 128 * 32; idx += FT_THREADS) {
-      const int r = idx >> 5, f4 = (idx & 31) * 4;
+    FT_DRAIN(2);
+    // all 16 row pieces of the thread loaded before any store (a load after a store to S
+    // cannot be hoisted by the compiler: one L2 round trip per piece, ~10k cycles per half)
+    constexpr int NPC = 128 * 32 / FT_THREADS;
+    float4 old[NPC];
+#pragma unroll
+    for (int k = 0; k < NPC; ++k) {
+      const int idx = tid + k * FT_THREADS, r = idx >> 5, f4 = (idx & 31) * 4;
+      old[k] = __ldcg(reinterpret_cast<const float4*>(S + (size_t)r * RANK + h * HALF + f4));
+    }
+#pragma unroll
+    for (int k = 0; k < NPC; ++k) {
+      const int idx = tid + k * FT_THREADS, r = idx >> 5, f4 = (idx & 31) * 4;
       const float4 t4 = *reinterpret_cast<const float4*>(tile + r * TLD + f4);
       const float4 z4 = *reinterpret_cast<const float4*>(ztv + f4);
-      float4* dst = reinterpret_cast<float4*>(S + (size_t)r * RANK + h * HALF + f4);
-      float4 o = *dst;
+      float4 o = old[k];
       o.x += t4.x + z4.x;
       o.y += t4.y + z4.y;
       o.z += t4.z + z4.z;
       o.w += t4.w + z4.w;
-      *dst = o;
+      *reinterpret_cast<float4*>(S + (size_t)r * RANK + h * HALF + f4) = o;
     }
+  }
+  FT_DRAIN(3);
   }
   tc::fence_before_sync();
   __syncthreads();
   FT_PHASE(3);
-  if (warp == 0) tc::tmem_dealloc(tb, FT_TMEM);
+  if (warp == 0) tc::tmem_dealloc(tb, npass == 2 ? FT_TMEM2 : FT_TMEM);
 }
 
-// W1k / W2k (fp32 [Hkv][128][128]) -> fp16 hi / lo B tiles of the phi GEMM,
-// [kvh][half][hi, lo][FT_TILE]: element (k = channel, n = feature).
-__global__ void prep_wtiles_kernel(kvlc_adapter ad, int Hkv, uint8_t* __restrict__ out) {
-  const int kvh = blockIdx.y, h = blockIdx.z;
-  const float* W = (h == 0 ? ad.w1k : ad.w2k) + (size_t)kvh * D * HALF;
-  uint8_t* hi = out + ((size_t)kvh * 2 + h) * 2 * FT_TILE;
-  uint8_t* lo = hi + FT_TILE;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D * HALF; i += gridDim.x * blockDim.x) {
-    const int ch = i / HALF, f = i % HALF;
-    __half x, y;
-    ft_hilo(W[i], x, y);
-    *reinterpret_cast<__half*>(hi + ft_off(f, ch)) = x;
-    *reinterpret_cast<__half*>(lo + ft_off(f, ch)) = y;
-  }
-}
 
 #ifdef KVLC_TRACE
 }  // namespace
@@ -1468,8 +1526,8 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
   KVLC_REQUIRE(s_part && wtiles && aimg && cimg && vsz, "flush workspace too small (%zu bytes)", ws_bytes);
   float* p_part = s_part + (size_t)units * splits * D * RANK;
   if (!direct) KVLC_CUDA(cudaMemsetAsync(s_part, 0, (size_t)units * splits * (D * RANK + RANK) * sizeof(float), s));
-  prep_wtiles_kernel<<<dim3(16, c->Hkv, 2), 256, 0, s>>>(*ad, c->Hkv, wtiles);
-  if ((rc = check_launch("prep_wtiles"))) return rc;
+  a.wtiles = wtiles;
+  a.prep_n = 16 * c->Hkv * 2;
   a.c = *c;
   a.ad = *ad;
   a.use_adapter = 1;
@@ -1496,7 +1554,13 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
   quant_kernel<<<dim3(max_nf, units, a.vsplit ? 1 + a.vsplit : 1), FT_THREADS, 0, s>>>(a, seq);
   if ((rc = check_launch("quant"))) return rc;
   KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
-  flush_tc_kernel<<<dim3(splits, units, 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
+  // one chunk per unit (decode-time ring flush): both feature halves in one CTA
+  static const int both_env = [] {
+    const char* e = getenv("KVLC_FT_BOTH");
+    return e ? atoi(e) : 1;
+  }();
+  a.both = (a.ring && max_nf == 1 && splits == 1 && both_env) ? 1 : 0;
+  flush_tc_kernel<<<dim3(splits, units, a.both ? 1 : 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
   if ((rc = check_launch("flush_tc"))) return rc;
   if (direct) return KVLC_OK;
   reduce_state_kernel<<<dim3(32, units), 256, 0, s>>>(*c, s_part, p_part, splits);
@@ -1646,7 +1710,9 @@ int kvlc_append(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* k_t
     a.v_t = 1;
     a.v_c = SLOTS;
     a.ring = 1;
+    a.finalize = 1;  // the ring counters move in flush_tc_kernel's first CTA
     if ((rc = launch_tc_flush(c, ad, a, seq, 1, KVLC_G, ws, ws_bytes, s))) return rc;
+    return KVLC_OK;
   } else if (any_flush) {
     const bool use_ad = adapter_on(ad);
     FlushArgs a{};

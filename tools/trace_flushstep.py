@@ -32,3 +32,9 @@ for h in range(2):
     r = buf[h, 39]
     print(f"half {h}: setup {r[1] - r[0]} cyc, chunk {r[2] - r[1]} cyc, drain {r[3] - r[2]} cyc "
           f"(total {(r[3] - r[0]) / 1965:.1f} us at 1965 MHz)")
+for h in range(2):
+    st = buf[h, :2]  # per-chunk stamps of the first chunk: 0 start, 1 phi issued, 2 phi done, 3 softmax done, 4 S issued
+    d = buf[h, 38]
+    print(f"half {h}: chunk phases (cyc from chunk start) phi {st[0][1] - st[0][0]}, phi done {st[0][2] - st[0][0]}, "
+          f"softmax done {st[0][3] - st[0][0]}, S issued {st[0][4] - st[0][0]}; drain: P {d[1] - d[0]}, "
+          f"tile {d[2] - d[1]}, rows {d[3] - d[2]} cyc")
