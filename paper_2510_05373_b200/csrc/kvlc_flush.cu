@@ -1332,26 +1332,31 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part, reinterpret_cast<uint32_t*>(z));
       tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part + 32, reinterpret_cast<uint32_t*>(z) + 32);
       tc::wait_ld();
-      float m = -INFINITY;
+      FT_STAMP(5);
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 chains (exact: max)
 #pragma unroll
-      for (int i = 0; i < 64; ++i) m = fmaxf(m, z[i]);
+      for (int i = 0; i < 64; ++i) m4[i & 3] = fmaxf(m4[i & 3], z[i]);
+      float m = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       sm.red[part][t] = m;
       __syncthreads();
       m = fmaxf(sm.red[0][t], sm.red[1][t]) * 1.4426950408889634f;
-      float ssum = 0.f;
+      FT_STAMP(6);
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 partial sums: a 64-deep add chain was latency
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
         float e2;
         asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(fmaf(z[i], 1.4426950408889634f, -m)));
         z[i] = e2;
-        ssum += e2;
+        s4[i & 3] += e2;
       }
+      const float ssum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
       __syncthreads();
       sm.red[part][t] = ssum;
       __syncthreads();
       const float inv = 1.f / (sm.red[0][t] + sm.red[1][t]);
       const float2 vz = sm.vsz[t];  // (s 2^e, z'): see quant_kernel
       const float sp = vz.x;
+      FT_STAMP(7);
       // B of the S GEMM: s' phi, element (token t, feature f); 8 consecutive features = 16 B
       float w[64];
 #pragma unroll
@@ -1367,6 +1372,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         *reinterpret_cast<uint4*>(sm.ps[0] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(hi);
         *reinterpret_cast<uint4*>(sm.ps[1] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(lo);
       }
+      FT_STAMP(8);
       // P and z^T Phi over the warp's 32 tokens: reduce-scatter (lane keeps features 2 lane + {0, 1})
 #pragma unroll
       for (int step = 0; step < 5; ++step) {
@@ -1382,6 +1388,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
           }
         }
       }
+      FT_STAMP(9);
       pacc[hp][0] += z[0];
       pacc[hp][1] += z[1];
       zacc[hp][0] += w[0];

@@ -38,3 +38,7 @@ for h in range(2):
     print(f"half {h}: chunk phases (cyc from chunk start) phi {st[0][1] - st[0][0]}, phi done {st[0][2] - st[0][0]}, "
           f"softmax done {st[0][3] - st[0][0]}, S issued {st[0][4] - st[0][0]}; drain: P {d[1] - d[0]}, "
           f"tile {d[2] - d[1]}, rows {d[3] - d[2]} cyc")
+for h in range(2):
+    st = buf[h, 0]
+    print(f"half {h} softmax steps (cyc from chunk start): tmem ld {st[5] - st[0]}, max+sync {st[6] - st[0]}, "
+          f"exp+sum+syncs {st[7] - st[0]}, hi/lo stores {st[8] - st[0]}, reduce-scatter {st[9] - st[0]}, done {st[3] - st[0]}")
