@@ -1157,17 +1157,21 @@ __global__ void __launch_bounds__(128) blocks_kernel(const kvlc_cache c, const f
 // tools/run_var.sh): config 2 (4 heads per group) 37.0 vs 36.8 us, config 4 29.7 vs 33.5 us,
 // config 3 (7 heads: 150+ registers, 3 CTAs per SM) 26.9-28.8 vs 24.9 us; so warp per chunk
 // for groups of <= 4 heads.  KVLC_WPC=0 / 1 forces either (A/B).
-bool wpc_on(int ng) {
+// Warp-per-chunk splits for a group of ng heads over `span` chunks per unit.  Groups of <= 4
+// heads always; larger groups (config 3's 7) from ~100 chunks: B16 x 16k 46.1 -> 44.7 us,
+// B64 x 16k 148.6 -> 143.8, B16 x 32k 76.8 -> 72.6, B64 x 32k 265.6 -> 243.4; shorter
+// contexts lose (B16 x 8k 26.7 -> 31.8, B16 x 4k 21.5 -> 22.5).  KVLC_WPC=0/1 forces.
+bool wpc_for(int ng, int span) {
   static const int v = [] {
     const char* e = getenv("KVLC_WPC");
     return e ? atoi(e) : -1;
   }();
-  return v < 0 ? ng <= 4 : v != 0;
+  return v < 0 ? (ng <= 4 || span >= 100) : v != 0;
 }
-int split_minb(int ng) { return wpc_on(ng) ? wpc_minb(ng) : KVLC_SPLIT_MINB; }
+int split_minb(int ng, bool wpc) { return wpc ? wpc_minb(ng) : KVLC_SPLIT_MINB; }
 
 struct Plan {
-  int NG, U, nsq, cpc, nrec, corr_on, rps, qrec;
+  int NG, U, nsq, cpc, nrec, corr_on, rps, qrec, wpc;
   size_t done_off, corr_off, rec_off, total;
 };
 
@@ -1184,7 +1188,8 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     return e ? atoi(e) : 0;
   }();
   int cpc = o && o->chunks_per_split > 0 ? o->chunks_per_split : cpc_env;
-  if (cpc == 0 && wpc_on(p.NG)) {
+  p.wpc = wpc_for(p.NG, span) ? 1 : 0;
+  if (cpc == 0 && p.wpc) {
     // warp per chunk: a split's 4 warps take every 4th chunk, so splits are sized in
     // whole chunks per warp (balanced warps; the CTA waits for its slowest warp before
     // merging).  About one wave of splits at WPC_MINB CTAs per SM, at most 52 records per
@@ -1210,7 +1215,7 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     // unit (the last CTA of a unit merges them all), then equal-length splits.
     // Configs 2 / 3 / 4: 7 -> 9 / 8 / 20 chunks, 49.2 -> 44.4 / 38.1 -> 34.8 / 55.6 -> 46.5 us.
     // Rounded (not ceiled) wave target: 64 chunks per unit get 8 x 8 rather than 6 x 10 + 4.
-    const long long slots = 148LL * split_minb(p.NG);
+    const long long slots = 148LL * split_minb(p.NG, p.wpc);
     const long long chunks = (long long)p.U * std::max(span, 1);
     long long t = std::max(8LL, (4 * chunks + 3 * slots) / (6 * slots));  // round(chunks / (1.5 slots))
     static const int rec_cap = [] {
@@ -1230,7 +1235,7 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     const char* e = getenv("KVLC_WARPREC");
     return e ? atoi(e) : 1;
   }();
-  p.rps = (warprec_env && wpc_on(p.NG) && 4 * p.nsq + (tail ? 2 : 0) <= 64) ? 4 : 1;
+  p.rps = (warprec_env && p.wpc && 4 * p.nsq + (tail ? 2 : 0) <= 64) ? 4 : 1;
   p.qrec = p.nsq * p.rps;
   p.nrec = p.qrec + (tail ? 2 : 0);
   size_t BH = (size_t)c->B * c->Hq;
@@ -1294,7 +1299,7 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     return e ? atoi(e) : 0;
   }();
   a.corr_split = corr_split_env ? corr_split_env
-                                : ((long long)p.U * (p.nsq + 1) > 148LL * split_minb(NG) ? 2 : 1);
+                                : ((long long)p.U * (p.nsq + 1) > 148LL * split_minb(NG, p.wpc) ? 2 : 1);
   // tail tasks: correction half h + residual half h in one CTA (one start-up and q staging
   // instead of two; both are latency-bound) when the correction runs in halves
   static const int tailfuse_env = [] {
@@ -1309,7 +1314,7 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   // two residual CTAs (B1 x 4k, 8 kv heads: NG 1 9.29 -> 8.59 us, NG 2 9.43 -> 9.26, NG 4
   // 10.29 -> 10.49, NG 4 at 32k 15.55 -> 14.65, NG 8 13.36 -> 16.43; Qwen NG 7 keeps fusing:
   // B1 x 32k 13.9 vs 15.3).  KVLC_TAILFUSE=0 off, 1 auto, 2 any group size.
-  const bool one_wave = (long long)p.U * (p.nsq + 2) <= 148LL * split_minb(NG);
+  const bool one_wave = (long long)p.U * (p.nsq + 2) <= 148LL * split_minb(NG, p.wpc);
   const bool fuse = tailfuse_env == 2 || (tailfuse_env == 1 && NG > 4);
   if (tail && p.corr_on && fuse && one_wave && !corr_split_env) a.corr_split = 2;
   a.tail_fused = tail && p.corr_on && a.corr_split == 2 && fuse && one_wave;
@@ -1324,9 +1329,9 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
   }();
   a.ntask = grid;
   a.queue = nullptr;
-  if (wpc_on(NG) && a.sep_combine && dyn_env) {
+  if (p.wpc && a.sep_combine && dyn_env) {
     a.queue = reinterpret_cast<uint32_t*>(ws + p.done_off) + p.U;
-    grid = std::min(grid, 148 * split_minb(NG));
+    grid = std::min(grid, 148 * split_minb(NG, true));
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -1349,7 +1354,7 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     return e ? atoi(e) & 3 : 3;
   }();
   const int extra = NG <= 4 ? 0 : extra_env;
-  if (wpc_on(NG)) {
+  if (p.wpc) {
     static bool attr_set[4] = {false, false, false, false};
     void (*kfn)(const DecArgs) = NG <= 4 || extra == 0 ? split_kernel_wpc<NG, 0>
                                  : extra == 1            ? split_kernel_wpc<NG, NG <= 4 ? 0 : 1>
