@@ -663,6 +663,14 @@ __device__ __forceinline__ void ft_hilo(float x, __half& hi, __half& lo) {
   hi = __float2half_rn(x);
   lo = __float2half_rn(x - __half2float(hi));
 }
+// ft_hilo of two values with packed conversions (the same bits: each half is rounded to nearest)
+__device__ __forceinline__ void ft_hilo2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
 __device__ __forceinline__ uint64_t ft_desc(const void* p) { return tc::bdesc(tc::smem_u32(p)); }
 
 // A tiles (A_phi = k_err [M = token][K = channel], A_S = Phi^T [M = feature][K = token]) in the
@@ -867,7 +875,7 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       for (int e = 0; e < 16; ++e) {
         const float4 pf = sm.kparf[ch0 + e];
         const float mnf = pf.x, scf = pf.y, invf = pf.z;
-        __half ehi[4], elo[4];
+        float kerr[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           uint32_t code = 0u;
@@ -880,13 +888,16 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
           // byte q of word t0 holds channel 16kt + 2t0 + {0,8,1,9}[q]; bit pair r holds token 4l + r
           const int t0 = (e & 7) >> 1, qb = ((e & 1) << 1) | (e >> 3);
           cw[t0] |= code << (8 * qb + 2 * r);
-          // k_err = k - (s code + z) (cache.py:153) as an fp16 hi / lo pair
-          ft_hilo(x[r][e] - fmaf((float)code, scf, mnf), ehi[r], elo[r]);
+          // k_err = k - (s code + z) (cache.py:153), stored as an fp16 hi / lo pair
+          kerr[r] = x[r][e] - fmaf((float)code, scf, mnf);
         }
         // A_phi image element (tokens 4l .. 4l+3, channel ch0 + e): 8 contiguous bytes
+        uint2 ehi, elo;
+        ft_hilo2(kerr[0], kerr[1], ehi.x, elo.x);
+        ft_hilo2(kerr[2], kerr[3], ehi.y, elo.y);
         const int off = ft_off_a(4 * lane, ch0 + e);
-        *reinterpret_cast<uint2*>(aimg + off) = *reinterpret_cast<const uint2*>(ehi);
-        *reinterpret_cast<uint2*>(aimg + FT_TILE + off) = *reinterpret_cast<const uint2*>(elo);
+        *reinterpret_cast<uint2*>(aimg + off) = ehi;
+        *reinterpret_cast<uint2*>(aimg + FT_TILE + off) = elo;
       }
       while (tie) {  // the exact fp64 decision (quantize.py:202-207) for the near-tie elements
         const int bit = __ffsll((long long)tie) - 1;
@@ -1361,16 +1372,17 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       float w[64];
 #pragma unroll
       for (int f8 = 0; f8 < 64; f8 += 8) {
-        __half hi[8], lo[8];
+        uint32_t hi[4], lo[4];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float ph = z[f8 + e] * inv;
           z[f8 + e] = ph;
           w[f8 + e] = vz.y * ph;
-          ft_hilo(sp * ph, hi[e], lo[e]);
         }
-        *reinterpret_cast<uint4*>(sm.ps[0] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(hi);
-        *reinterpret_cast<uint4*>(sm.ps[1] + ft_off(64 * part + f8, t)) = *reinterpret_cast<uint4*>(lo);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ft_hilo2(sp * z[f8 + 2 * e], sp * z[f8 + 2 * e + 1], hi[e], lo[e]);
+        *reinterpret_cast<uint4*>(sm.ps[0] + ft_off(64 * part + f8, t)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(sm.ps[1] + ft_off(64 * part + f8, t)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
       FT_STAMP(8);
       // P and z^T Phi over the warp's 32 tokens: reduce-scatter (lane keeps features 2 lane + {0, 1})
