@@ -288,9 +288,10 @@ int kvlc_decode(const kvlc_cache* cache, const kvlc_adapter* ad,
  * (attention.py:41-47, 197-276): the fused decode (out as kvlc_decode) plus, per (b, q-head),
  * its per-block partials in blocks [B][Hq][max_blocks][2 + 128] fp32 = (block max m in natural
  * logit units, block sum l = sum exp(s - m), y = sum exp(s - m) v in the stored basis): the
- * n_chunks[b] quantized blocks, then the residual window as one block; rows past a sequence's
- * blocks are zero.  max_blocks >= max n_chunks + 1.  Workspace: kvlc_decode_workspace() with
- * chunks_per_split = 1. */
+ * ceil(n_chunks[b] / c) quantized blocks of block_tokens = c G (c = o->chunks_per_split, 1 when
+ * 0: block_tokens = G), then the residual window as one block; rows past a sequence's blocks are
+ * zero.  max_blocks >= ceil(max n_chunks / c) + 1.  Workspace: kvlc_decode_workspace() with
+ * chunks_per_split = c. */
 int kvlc_decode_blocks(const kvlc_cache* cache, const kvlc_adapter* ad, const uint16_t* q,
                        void* out, float* blocks, int32_t max_blocks, const kvlc_decode_opts* o,
                        void* ws, size_t ws_bytes, void* stream);

@@ -275,27 +275,37 @@ class BatchedKVCache:
                   ctypes.byref(o), _ptr(ws), ws.numel(), _lib.stream_handle())
         return out
 
-    def decode_blocks(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False):
-        """decode_step_blocked(..., return_partials=True) at block_tokens = G for every (b, q-head)
+    def decode_blocks(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False,
+                      block_tokens: int | None = None):
+        """decode_step_blocked(..., block_tokens, return_partials=True) for every (b, q-head)
         (attention.py:41-47, 197-276; kvlc_decode_blocks): returns (out float32 [B, Hq, 128],
         partials) with partials = dict(y [B, Hq, NB, 128] stored basis, m [B, Hq, NB] block max
         in natural logit units, l [B, Hq, NB] block sums, n_blocks [B]) -- the quantized blocks
-        then the residual window as one block; rows past a sequence's n_blocks are zero."""
+        then the residual window as one block; rows past a sequence's n_blocks are zero.  The
+        serving cache's blocks are whole chunks: block_tokens a multiple of G (default G); the
+        per-head shim (attention.decode_step_blocked) takes any block size."""
         if q.shape != (self.B, self.Hq, D):
             raise ValueError(f"query shape {tuple(q.shape)} != ({self.B}, {self.Hq}, {D})")
         if np.any(self.tokens == 0):
             raise ValueError("cannot decode against an empty cache")
+        block = G if block_tokens is None else int(block_tokens)
+        if block < 1:
+            raise ValueError(f"block_tokens must be >= 1, got {block}")
+        if block % G:
+            raise ValueError(f"the serving cache decodes whole chunks: block_tokens must be a multiple of {G}, "
+                             f"got {block}")
+        cpb = block // G
         q = q.to(self.device, torch.bfloat16).contiguous()
         out = torch.empty(q.shape, dtype=torch.float32, device=self.device)
-        nb = int(self.n_chunks.max()) + 1
+        nb = -(-int(self.n_chunks.max()) // cpb) + 1
         blocks = torch.zeros((self.B, self.Hq, nb, 2 + D), dtype=torch.float32, device=self.device)
-        o = self._opts(literal, 1, True)
+        o = self._opts(literal, cpb, True)
         nbytes = _lib.load().kvlc_decode_workspace(ctypes.byref(self._struct), ctypes.byref(o))
         ws = self.decode_ws(nbytes)
         ad = _adapter_struct(adapters)
         _lib.call("kvlc_decode_blocks", ctypes.byref(self._struct), ctypes.byref(ad), _ptr(q), _ptr(out),
                   _ptr(blocks), nb, ctypes.byref(o), _ptr(ws), ws.numel(), _lib.stream_handle())
-        n_blocks = self.n_chunks + (self.res_len > 0)
+        n_blocks = -(-self.n_chunks // cpb) + (self.res_len > 0)
         return out, {"m": blocks[..., 0], "l": blocks[..., 1], "y": blocks[..., 2:], "n_blocks": n_blocks}
 
     def capture_decode(self, q: torch.Tensor, adapters: AdapterBank | None = None, literal: bool = False,

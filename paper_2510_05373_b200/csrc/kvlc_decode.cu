@@ -1107,15 +1107,17 @@ __global__ void __launch_bounds__(128) merge_records_kernel(const float* __restr
 }
 
 // Per-block partials of decode_step_blocked (return_partials, attention.py:41-47, 269-275) from
-// the records of a one-chunk-per-split decode: block i < n_chunks (the quantized blocks of
-// G tokens, stored basis) and one residual block (the two ring halves merged), converted from
-// the kernel's log2-unit reference points to the reference's natural-unit block max:
-// m = m_true ln 2, l and y scaled by 2^(m_ref - m_true).  out: [B][Hq][max_blocks][2 + D].
+// the records of a decode whose splits are the blocks (cpc chunks each): block i < ceil(n_chunks /
+// cpc) (the quantized blocks of cpc G tokens, stored basis; a split's rps warp records merged) and
+// one residual block (the two ring halves merged), converted from the kernel's log2-unit
+// reference points to the reference's natural-unit block max: m = m_true ln 2, l and y scaled
+// by 2^(m_ref - m_true).  out: [B][Hq][max_blocks][2 + D].
 __global__ void __launch_bounds__(128) blocks_kernel(const kvlc_cache c, const float* __restrict__ rec, int nrec,
-                                                     int nsq, int rps, int NG, int max_blocks, float* __restrict__ out) {
+                                                     int nsq, int rps, int cpc, int NG, int max_blocks,
+                                                     float* __restrict__ out) {
   const int gw = blockIdx.x, b = gw / c.Hq, qh = gw % c.Hq, kvh = qh / NG, hl = qh % NG;
   const int unit = b * c.Hkv + kvh;
-  const int nq = min(c.n_chunks[b], nsq), has_res = c.res_len[b] > 0 ? 1 : 0;
+  const int nq = min((c.n_chunks[b] + cpc - 1) / cpc, nsq), has_res = c.res_len[b] > 0 ? 1 : 0;
   const size_t rs = (size_t)NG * REC;
   const float* base = rec + ((size_t)unit * nrec * NG + hl) * REC;
   float* o = out + (size_t)gw * max_blocks * (2 + D);
@@ -1123,8 +1125,26 @@ __global__ void __launch_bounds__(128) blocks_kernel(const kvlc_cache c, const f
   for (int i = 0; i < max_blocks; ++i) {
     float m = 0.f, l = 0.f, f0 = 0.f, f1 = 0.f;
     const float *y0 = nullptr, *y1 = nullptr;
+    if (i < nq && rps > 1) {  // a block of several warp records: merged at the block's true max
+      const float* r = base + (size_t)i * rps * rs;
+      float M = -INFINITY;
+      for (int w = 0; w < rps; ++w) M = fmaxf(M, r[w * rs + 2]);
+      float y = 0.f;
+      for (int w = 0; w < rps; ++w) {
+        const float* rw = r + w * rs;
+        const float f = rw[0] == -INFINITY ? 0.f : exp2f(rw[0] - M);
+        l = fmaf(rw[1], f, l);
+        y = fmaf(rw[4 + threadIdx.x], f, y);
+      }
+      if (threadIdx.x == 0) {
+        o[i * (2 + D)] = M * LN2;
+        o[i * (2 + D) + 1] = l;
+      }
+      o[i * (2 + D) + 2 + threadIdx.x] = y;
+      continue;
+    }
     if (i < nq) {
-      const float* r = base + (size_t)i * rps * rs;  // one chunk per split: warp 0's record
+      const float* r = base + (size_t)i * rps * rs;  // one record per block
       f0 = r[2] == -INFINITY ? 0.f : exp2f(r[0] - r[2]);
       m = r[2] * LN2;
       l = r[1] * f0;
@@ -1447,7 +1467,8 @@ int kvlc_decode_blocks(const kvlc_cache* c, const kvlc_adapter* ad, const uint16
   KVLC_REQUIRE(q && out && blocks, "null query / output / blocks");
   kvlc_decode_opts o1{};
   if (o) o1 = *o;
-  o1.chunks_per_split = 1;  // one record per quantized chunk = one block of G tokens
+  // a split per block: block_tokens = chunks_per_split x G (default one chunk)
+  if (o1.chunks_per_split <= 0) o1.chunks_per_split = 1;
   Plan p{};
   int rc = plan_for(c, &o1, 0, 1 << 30, 1, adapter_active(ad), p);
   if (rc) return rc;
@@ -1458,8 +1479,8 @@ int kvlc_decode_blocks(const kvlc_cache* c, const kvlc_adapter* ad, const uint16
               as_stream(stream));
   if (rc) return rc;
   blocks_kernel<<<c->B * c->Hq, 128, 0, as_stream(stream)>>>(
-      *c, reinterpret_cast<const float*>(static_cast<char*>(ws) + p.rec_off), p.nrec, p.nsq, p.rps, p.NG, max_blocks,
-      blocks);
+      *c, reinterpret_cast<const float*>(static_cast<char*>(ws) + p.rec_off), p.nrec, p.nsq, p.rps, p.cpc, p.NG,
+      max_blocks, blocks);
   return check_launch("decode_blocks");
 }
 

@@ -442,10 +442,10 @@ def test_captured_decode_refuses_a_changed_cache():
         g.replay()
 
 
-@pytest.mark.parametrize("Hq", [4, 8])
-def test_decode_blocks_match_reference_partials(Hq):
-    """return_partials on the serving cache (kvlc_decode_blocks, block_tokens = G): per-block
-    (max, sum, y) against decode_step_blocked's DecodePartial on the oracle cache."""
+@pytest.mark.parametrize("Hq,block", [(4, None), (8, None), (4, 256), (4, 384), (8, 512)])
+def test_decode_blocks_match_reference_partials(Hq, block):
+    """return_partials on the serving cache (kvlc_decode_blocks, block_tokens = G or a multiple):
+    per-block (max, sum, y) against decode_step_blocked's DecodePartial on the oracle cache."""
     B, Hkv, n = 2, 2, 900
     lens = [900, 700]
     k, v, q = make_inputs(B, Hkv, Hq, n, seed=61)
@@ -453,7 +453,7 @@ def test_decode_blocks_match_reference_partials(Hq):
     bank = AdapterBank.initialize(Hkv)
     cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
     cache.prefill(tdev(k), tdev(v), lens=lens, adapters=bank)
-    out, part = cache.decode_blocks(tdev(q), adapters=bank)
+    out, part = cache.decode_blocks(tdev(q), adapters=bank, block_tokens=block)
     full = cache.decode(tdev(q), adapters=bank, out_dtype=F32)
     assert (out - full).abs().max().item() <= 2e-4 * full.abs().max().item()
     ocs = oracle_caches(k, v, lens, oads)
@@ -462,7 +462,8 @@ def test_decode_blocks_match_reference_partials(Hq):
         nbk = int(part["n_blocks"][b])
         for h in range(Hq):
             oc = orc.fp16_meta_copy(ocs[b][h // NG])
-            _, (ry, rm, rl) = orc.decode_blocked(q[b, h].astype(np.float64), oc, oads[h // NG], return_partials=True)
+            _, (ry, rm, rl) = orc.decode_blocked(q[b, h].astype(np.float64), oc, oads[h // NG], block=block,
+                                                 return_partials=True)
             assert len(rm) == nbk
             m = part["m"][b, h, :nbk].cpu().numpy()
             l = part["l"][b, h, :nbk].cpu().numpy()
@@ -471,3 +472,12 @@ def test_decode_blocks_match_reference_partials(Hq):
             assert np.abs(l - rl).max() <= 2e-4 * np.abs(rl).max(), (b, h)
             assert np.abs(y - ry).max() <= 1e-3 * np.abs(ry).max(), (b, h)
             assert not part["y"][b, h, nbk:].any()
+
+
+def test_decode_blocks_rejects_partial_chunks():
+    cache = BatchedKVCache(1, 1, 4, max_tokens=512)
+    k, v, _ = make_inputs(1, 1, 4, 300, seed=3)
+    cache.prefill(tdev(k), tdev(v))
+    q = torch.zeros(1, 4, D, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="multiple of 128"):
+        cache.decode_blocks(q, block_tokens=200)
