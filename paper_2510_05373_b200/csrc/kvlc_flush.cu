@@ -1308,30 +1308,30 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   // lane owns features 64 part + 2 lane + {0, 1} (reduce-scatter order)
   float pacc[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, zacc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
   FT_PHASE(1);
-  if (npass == 2 && c_hi - c_lo != 1) __trap();  // both halves: the A / code tiles stay resident
-
+  // pass pi: chunk ci = c_lo + pi / npass, half h0 + hp (hp = pi % npass).  Barrier phases: the
+  // A / code tiles complete once per chunk (ic), the phi / S GEMMs once per pass (it = pi)
   for (int pi = 0; pi < npass * (c_hi - c_lo); ++pi) {
-    // pass pi: chunk ci, half h0 + hp (both: pi = hp over the one chunk; else pi = it)
-    const int hp = npass == 2 ? pi : 0, ci = c_lo + (npass == 2 ? 0 : pi), it = pi;
+    const int hp = pi % npass, ic = pi / npass, ci = c_lo + ic, it = pi;
     FT_STAMP(0);
     if (warp == 0) {  // phi GEMM: Z = k_err W_h (passes hi.hi, hi.lo once A hi has landed, lo.hi after A lo)
-      if (hp == 0) tc::mbar_wait(&sm.ma[0], (uint32_t)it & 1u);
+      if (hp == 0) tc::mbar_wait(&sm.ma[0], (uint32_t)ic & 1u);
       tc::fence_after_sync();
       ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false, hp == 0 ? &sm.ma[1] : nullptr,
-              (uint32_t)it & 1u, 2);
+              (uint32_t)ic & 1u, 2);
       tc::mma_commit_w(&sm.mphi);
     }
     FT_STAMP(1);
     tc::mbar_wait(&sm.mphi, (uint32_t)it & 1u);
     tc::fence_after_sync();
-    if (tid == 0 && ci + 1 < c_hi) ft_load_a(sm, a, slot0 + ci + 1);  // A_phi consumed: next one in flight
-    if (npass == 2 && hp == 0) {  // W of the second half into the freed W tiles (lands during the softmax)
-      const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + 1) * 2 * FT_TILE);
+    // A_phi consumed by the chunk's last pass: the next chunk's in flight
+    if (tid == 0 && hp == npass - 1 && ci + 1 < c_hi) ft_load_a(sm, a, slot0 + ci + 1);
+    if (npass == 2 && pi + 1 < npass * (c_hi - c_lo)) {  // the other half's W into the freed W tiles
+      const uint4* src = reinterpret_cast<const uint4*>(wtiles + ((size_t)kvh * 2 + (1 - hp)) * 2 * FT_TILE);
       uint4* dst = reinterpret_cast<uint4*>(sm.w[0]);
       for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
       tc::cp_commit();
     }
-    if (hp == 0) tc::mbar_wait(&sm.mc, (uint32_t)it & 1u);  // this chunk's (s, z)
+    if (hp == 0) tc::mbar_wait(&sm.mc, (uint32_t)ic & 1u);  // this chunk's codes and (s, z)
     if (it > 0) tc::mbar_wait(&sm.ms, (uint32_t)(it - 1) & 1u);  // the previous S GEMM has read s' Phi
     FT_STAMP(2);
 
@@ -1406,16 +1406,16 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       zacc[hp][0] += w[0];
       zacc[hp][1] += w[1];
     }
-    if (npass == 2 && hp == 0) tc::cp_wait<0>();  // second half's W (before the barrier below)
+    if (npass == 2) tc::cp_wait<0>();  // the next pass's W (before the barrier below)
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
     FT_STAMP(3);
     if (warp == 0) {  // S GEMM: D^T += codes^T (s' Phi), then the next code tile once it is read
       tc::fence_after_sync();
-      ft_gemm_s(tb + FT_COL_S + 128 * hp, sm.cv, sm.ps[0], sm.ps[1], npass == 1 && it > 0);
+      ft_gemm_s(tb + FT_COL_S + 128 * hp, sm.cv, sm.ps[0], sm.ps[1], ic > 0);
       tc::mma_commit_w(&sm.ms);
-      if (ci + 1 < c_hi) {
+      if (hp == npass - 1 && ci + 1 < c_hi) {
         tc::mbar_wait(&sm.ms, (uint32_t)it & 1u);
         if (lane == 0) ft_load_c(sm, a, slot0 + ci + 1);
         __syncwarp();
@@ -1540,9 +1540,14 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
 #ifndef KVLC_TC_MAXCPC
 #define KVLC_TC_MAXCPC 32
 #endif
-  const int base = std::max({1, std::min(max_nf, sms / (2 * units)), (max_nf + KVLC_TC_MAXCPC - 1) / KVLC_TC_MAXCPC});
-  const int waves = (2 * units * base + sms - 1) / sms;  // one CTA per SM: fill the last wave
-  const int splits = std::min({ws_splits, std::max(1, max_nf), std::max(base, waves * sms / (2 * units))});
+  static const int both_env = [] {  // KVLC_FT_BOTH: 0 off, 1 ring flushes (default), 2 always
+    const char* e = getenv("KVLC_FT_BOTH");
+    return e ? atoi(e) : 1;
+  }();
+  const int per = both_env == 2 ? 1 : 2;  // state CTAs per (unit, chunk range)
+  const int base = std::max({1, std::min(max_nf, sms / (per * units)), (max_nf + KVLC_TC_MAXCPC - 1) / KVLC_TC_MAXCPC});
+  const int waves = (per * units * base + sms - 1) / sms;  // one CTA per SM: fill the last wave
+  const int splits = std::min({ws_splits, std::max(1, max_nf), std::max(base, waves * sms / (per * units))});
   const int cpc = (max_nf + splits - 1) / splits;
   // one CTA per (unit, feature half): it adds its S / P straight into the cache (the halves
   // write disjoint columns), no partials, memset or reduction (decode-time ring flushes)
@@ -1586,11 +1591,7 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
   if ((rc = check_launch("quant"))) return rc;
   KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
   // one chunk per unit (decode-time ring flush): both feature halves in one CTA
-  static const int both_env = [] {
-    const char* e = getenv("KVLC_FT_BOTH");
-    return e ? atoi(e) : 1;
-  }();
-  a.both = (a.ring && max_nf == 1 && splits == 1 && both_env) ? 1 : 0;
+  a.both = (both_env == 2 || (a.ring && max_nf == 1 && splits == 1 && both_env)) ? 1 : 0;
   flush_tc_kernel<<<dim3(splits, units, a.both ? 1 : 2), FT_THREADS, sizeof(FtSmem), s>>>(a, seq, wtiles);
   if ((rc = check_launch("flush_tc"))) return rc;
   if (direct) return KVLC_OK;
