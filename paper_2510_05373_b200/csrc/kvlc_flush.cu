@@ -663,6 +663,20 @@ __device__ __forceinline__ void ft_hilo(float x, __half& hi, __half& lo) {
   hi = __float2half_rn(x);
   lo = __float2half_rn(x - __half2float(hi));
 }
+// P / z'^T Phi on the tensor cores (legacy warp MMA): D[r][f] = sum_t A[r][t] B[t][f] with B =
+// s' Phi hi / lo (the S GEMM's B tile) and the 4 nonzero rows of A = 2^10 / s'_t and 2^10 z'_t / s'_t
+// as fp16 hi / lo, so P = (D0 + D1) 2^-10 and z'^T Phi = (D2 + D3) 2^-10 (a lane reduce-scatter of
+// 2 x 64 values per token thread cost ~1.3 K cycles per pass)
+__device__ __forceinline__ void ft_ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ft_mma16816(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
 // ft_hilo of two values with packed conversions (the same bits: each half is rounded to nearest)
 __device__ __forceinline__ void ft_hilo2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
@@ -1164,7 +1178,11 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
           auto hc = [&](uint32_t cd) { return (uint32_t)__half_as_ushort(__float2half_rn(((float)cd - 1.5f) * cs)); };
           *reinterpret_cast<uint2*>(a.cimg + slot * FT_TILE + ft_off(4 * lane, t)) =
               make_uint2(hc(code[0]) | (hc(code[1]) << 16), hc(code[2]) | (hc(code[3]) << 16));
-          if (lane == 0) a.vsz[slot * G + t] = make_float2(vsc * __int_as_float((127 + e) << 23), vmid);
+          // a constant row (s = 0, codes 0) is stored as s = 1, z' = z + 3/2: the same
+          // (code - 3/2) s + z' = z, and the state kernel's 1 / s' exists
+          if (lane == 0)
+            a.vsz[slot * G + t] = vsc > 0.f ? make_float2(vsc * __int_as_float((127 + e) << 23), vmid)
+                                            : make_float2(__int_as_float((127 + e) << 23), vmid + 1.5f);
         }
         if (writer && lane == 0) {
           c.vscale[cb * G + t] = meta_s;
@@ -1306,7 +1324,13 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   const int part = warp >> 2;
   // P[f] = sum_t phi[t][f], Z[f] = sum_t z_t phi[t][f] for this warp's 32 token rows:
   // lane owns features 64 part + 2 lane + {0, 1} (reduce-scatter order)
-  float pacc[2][2] = {{0.f, 0.f}, {0.f, 0.f}}, zacc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+  // MMA accumulators of the P / z'^T Phi rows per half (pz0, pz1) and n-tile (registers: the
+  // half is selected by a branch, not an index)
+  float pz0[2][4], pz1[2][4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) pz0[j][e] = pz1[j][e] = 0.f;
   FT_PHASE(1);
   // pass pi: chunk ci = c_lo + pi / npass, half h0 + hp (hp = pi % npass).  Barrier phases: the
   // A / code tiles complete once per chunk (ic), the phi / S GEMMs once per pass (it = pi)
@@ -1367,60 +1391,82 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       const float inv = 1.f / (sm.red[0][t] + sm.red[1][t]);
       const float2 vz = sm.vsz[t];  // (s 2^e, z'): see quant_kernel
       const float sp = vz.x;
+      __syncthreads();  // every thread has read the softmax sums: red takes the P / Z A rows
+      if (part == 0) {  // token t: (2^10 / s', 2^10 z' / s') as fp16 hi / lo pairs
+        const float is = __frcp_rn(sp) * 1024.f;
+        uint32_t hi2, lo2;
+        ft_hilo2(is, vz.y * is, hi2, lo2);
+        uint32_t* tbl = reinterpret_cast<uint32_t*>(sm.red);
+        tbl[t] = __byte_perm(hi2, lo2, 0x5410);        // (inv hi, inv lo)
+        tbl[G + t] = __byte_perm(hi2, lo2, 0x7632);    // (z' inv hi, z' inv lo)
+      }
       FT_STAMP(7);
       // B of the S GEMM: s' phi, element (token t, feature f); 8 consecutive features = 16 B
-      float w[64];
 #pragma unroll
       for (int f8 = 0; f8 < 64; f8 += 8) {
         uint32_t hi[4], lo[4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float ph = z[f8 + e] * inv;
-          z[f8 + e] = ph;
-          w[f8 + e] = vz.y * ph;
-        }
+        for (int e = 0; e < 8; ++e) z[f8 + e] *= inv;
 #pragma unroll
         for (int e = 0; e < 4; ++e) ft_hilo2(sp * z[f8 + 2 * e], sp * z[f8 + 2 * e + 1], hi[e], lo[e]);
         *reinterpret_cast<uint4*>(sm.ps[0] + ft_off(64 * part + f8, t)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(sm.ps[1] + ft_off(64 * part + f8, t)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
       FT_STAMP(8);
-      // P and z^T Phi over the warp's 32 tokens: reduce-scatter (lane keeps features 2 lane + {0, 1})
-#pragma unroll
-      for (int step = 0; step < 5; ++step) {
-        const int sft = 16 >> step, n = 32 >> step;
-        const bool up = lane & sft;
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          if (e < n) {
-            const float s1 = up ? z[e] : z[e + n], k1 = up ? z[e + n] : z[e];
-            const float s2 = up ? w[e] : w[e + n], k2 = up ? w[e + n] : w[e];
-            z[e] = k1 + __shfl_xor_sync(0xffffffffu, s1, sft);
-            w[e] = k2 + __shfl_xor_sync(0xffffffffu, s2, sft);
-          }
-        }
-      }
       FT_STAMP(9);
-      pacc[hp][0] += z[0];
-      pacc[hp][1] += z[1];
-      zacc[hp][0] += w[0];
-      zacc[hp][1] += w[1];
     }
     if (npass == 2) tc::cp_wait<0>();  // the next pass's W (before the barrier below)
     tc::fence_proxy_async();
     tc::fence_before_sync();
     __syncthreads();
     FT_STAMP(3);
-    if (warp == 0) {  // S GEMM: D^T += codes^T (s' Phi), then the next code tile once it is read
+    if (warp == 0) {  // S GEMM: D^T += codes^T (s' Phi)
       tc::fence_after_sync();
       ft_gemm_s(tb + FT_COL_S + 128 * hp, sm.cv, sm.ps[0], sm.ps[1], ic > 0);
       tc::mma_commit_w(&sm.ms);
-      if (hp == npass - 1 && ci + 1 < c_hi) {
-        tc::mbar_wait(&sm.ms, (uint32_t)it & 1u);
-        if (lane == 0) ft_load_c(sm, a, slot0 + ci + 1);
-        __syncwarp();
-      }
     }
+    // this warp's 16 features (two n-tiles) over the chunk's 128 tokens, into a fresh accumulator
+    // added to the running total with round-to-nearest adds (the MMA's truncating accumulation
+    // over all chunks drifted P to 2.7e-5 relative at 8k tokens, T3 is 1e-5)
+    auto pz_mma = [&](float (&tot)[2][4]) {
+      float pz[2][4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) pz[j][0] = pz[j][1] = pz[j][2] = pz[j][3] = 0.f;
+      const uint32_t* tbl = reinterpret_cast<const uint32_t*>(sm.red);
+      const int g = lane >> 2, t4 = lane & 3, mi = lane >> 3, fb = 16 * warp;
+      const uint32_t sel = (g & 1) ? 0x7632u : 0x5410u;  // hi or lo half of the (hi, lo) pairs
+      const uint32_t* trow = tbl + ((g >> 1) & 1) * G;
+#pragma unroll 2
+      for (int k0 = 0; k0 < G; k0 += 16) {
+        uint32_t a0 = 0u, a2 = 0u;
+        if (g < 4) {
+          a0 = __byte_perm(trow[k0 + 2 * t4], trow[k0 + 2 * t4 + 1], sel);
+          a2 = __byte_perm(trow[k0 + 2 * t4 + 8], trow[k0 + 2 * t4 + 9], sel);
+        }
+        const int tok = k0 + (mi & 1) * 8 + (lane & 7), fe = fb + (mi >> 1) * 8;
+        uint32_t bh[4], bl[4];
+        ft_ldsm_x4_t(tc::smem_u32(sm.ps[0] + ft_off(fe, tok)), bh);
+        ft_ldsm_x4_t(tc::smem_u32(sm.ps[1] + ft_off(fe, tok)), bl);
+        ft_mma16816(pz[0], a0, a2, bh[0], bh[1]);
+        ft_mma16816(pz[1], a0, a2, bh[2], bh[3]);
+        ft_mma16816(pz[0], a0, a2, bl[0], bl[1]);
+        ft_mma16816(pz[1], a0, a2, bl[2], bl[3]);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) tot[j][e] += pz[j][e];
+    };
+    if (hp == 0)
+      pz_mma(pz0);
+    else
+      pz_mma(pz1);
+    if (warp == 0 && hp == npass - 1 && ci + 1 < c_hi) {  // the next code tile once this one is read
+      tc::mbar_wait(&sm.ms, (uint32_t)it & 1u);
+      if (lane == 0) ft_load_c(sm, a, slot0 + ci + 1);
+      __syncwarp();
+    }
+    __syncthreads();  // the A rows (red) and s' Phi reads are done before the next pass writes them
     FT_STAMP(4);
   }
 
@@ -1433,20 +1479,25 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   const int h = h0 + hp;
   if (hp > 0) __syncthreads();  // the previous half's tile / row reads are done
   FT_DRAIN(0);
-  float* zf = reinterpret_cast<float*>(sm.ps[0]);  // free now: [4 token groups][128 features][P, Z]
+  float* zf = reinterpret_cast<float*>(sm.ps[0]);  // free now: [P | z'^T Phi][128 features]
   {
-    const int f = 64 * part + 2 * lane;
-    *reinterpret_cast<float4*>(zf + ((warp & 3) * 128 + f) * 2) =
-        make_float4(pacc[hp][0], zacc[hp][0], pacc[hp][1], zacc[hp][1]);
+    const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float x = hp == 0 ? pz0[nt][e] : pz1[nt][e];
+        const float v = x + __shfl_xor_sync(0xffffffffu, x, 4);  // hi + lo rows
+        const int f = 16 * warp + 8 * nt + 2 * t4 + e;
+        if (g == 0) zf[f] = v * (1.f / 1024.f);
+        if (g == 2) zf[G + f] = v * (1.f / 1024.f);
+      }
   }
   __syncthreads();
   float* S = a.s_out ? a.s_out + ((size_t)unit * a.splits + split) * D * RANK : c.S + (size_t)unit * D * RANK;
   float* P = a.p_out ? a.p_out + ((size_t)unit * a.splits + split) * RANK : c.P + (size_t)unit * RANK;
   if (tid < HALF) {
-    float pf = 0.f;
-#pragma unroll
-    for (int g4 = 0; g4 < 4; ++g4) pf += zf[(g4 * 128 + tid) * 2];
-    P[h * HALF + tid] += pf;
+    P[h * HALF + tid] += zf[tid];
   }
   FT_DRAIN(1);
   // S rows: TMEM -> a padded shared tile (the W / A tiles are free now) -> coalesced 16-B
@@ -1471,8 +1522,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     }
     if (tid < HALF) {
       const int f = tid;
-      ztv[f] = (zf[(0 * 128 + f) * 2 + 1] + zf[(1 * 128 + f) * 2 + 1]) +
-               (zf[(2 * 128 + f) * 2 + 1] + zf[(3 * 128 + f) * 2 + 1]);
+      ztv[f] = zf[G + f];
     }
     __syncthreads();
     FT_DRAIN(2);
