@@ -481,3 +481,29 @@ def test_decode_blocks_rejects_partial_chunks():
     q = torch.zeros(1, 4, D, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError, match="multiple of 128"):
         cache.decode_blocks(q, block_tokens=200)
+
+
+def test_constant_value_rows_prefill_and_ring_flush():
+    """Value rows whose channels are all equal (scale 0, codes 0): bit-exact metadata and the
+    adapter state within T3 on the prefill path and on a decode-time ring flush (the state
+    kernel stores such rows as s = 1, z' = z + 3/2 for its P / z'^T Phi MMA)."""
+    B, Hkv, Hq, n = 1, 2, 8, 700
+    k, v, q = make_inputs(B, Hkv, Hq, n, seed=29)
+    # rows that are constant AFTER the value rotation: multiples of a unit vector (H e_0 is
+    # flat) and zero rows
+    v[:, :, 5:45, :] = 0.0
+    v[:, :, 5:40, 0] = 0.5
+    v[:, :, 300:330, :] = 0.0
+    v[:, :, 300:330, 0] = -1.25
+    oads = [orc.init_adapter(D, 256, seed=h) for h in range(Hkv)]
+    bank = AdapterBank.initialize(Hkv)
+    cache = BatchedKVCache(B, Hkv, Hq, max_tokens=n + 256)
+    cache.prefill(tdev(k[:, :, :600]), tdev(v[:, :, :600]), adapters=bank)
+    for i in range(600, n):
+        cache.append(tdev(k[:, :, i]), tdev(v[:, :, i]), adapters=bank)
+    ocs = oracle_caches(k, v, [n], oads)
+    check_cache_exact(cache, ocs, [n])
+    check_states(cache, ocs)
+    out = cache.decode(tdev(q), adapters=bank, out_dtype=F32).cpu().numpy()
+    ref = oracle_decode(q, ocs, oads)
+    assert np.abs(out - ref).max() <= 1e-3 * np.abs(ref).max()
