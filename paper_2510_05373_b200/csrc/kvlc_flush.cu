@@ -624,7 +624,8 @@ __global__ void deserialize_unit_kernel(kvlc_cache c, int unit, int n, int n_res
 //       end.  The next chunk's A_phi image streams in while the softmax and S GEMM run.
 constexpr int FT_THREADS = 256;
 constexpr int FT_TILE = 32768;              // [128][128] fp16 tile
-constexpr uint32_t FT_COL_PHI = 0, FT_COL_S = 128, FT_TMEM = 256, FT_TMEM2 = 512;  // 2: S of both halves
+// TMEM columns: phi of even passes, S (half 0), S (half 1 of a two-halves CTA), phi of odd passes
+constexpr uint32_t FT_COL_PHI = 0, FT_COL_S = 128, FT_COL_PHI1 = 384, FT_TMEM2 = 512;
 constexpr uint32_t FT_IDESC_PHI = (1u << 4) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | (8u << 24);
 
 struct FtSmem {
@@ -1303,7 +1304,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     for (int i = tid; i < 2 * FT_TILE / 16; i += FT_THREADS) tc::cp_async16(dst + i, src + i);
     tc::cp_commit();
   }
-  if (warp == 0) tc::tmem_alloc(&sm.tbase, npass == 2 ? FT_TMEM2 : FT_TMEM);
+  if (warp == 0) tc::tmem_alloc(&sm.tbase, FT_TMEM2);
   if (tid == 0) {
     tc::mbar_init(&sm.mphi, 1);
     tc::mbar_init(&sm.ms, 1);
@@ -1334,16 +1335,24 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   FT_PHASE(1);
   // pass pi: chunk ci = c_lo + pi / npass, half h0 + hp (hp = pi % npass).  Barrier phases: the
   // A / code tiles complete once per chunk (ic), the phi / S GEMMs once per pass (it = pi)
-  for (int pi = 0; pi < npass * (c_hi - c_lo); ++pi) {
+  // phi GEMM of pass q: Z = k_err W_h into the pass's phi columns (hi.hi, hi.lo once A hi has
+  // landed, lo.hi after A lo).  Pass 0's is issued here; pass q + 1's right after pass q's S GEMM,
+  // so it runs on the tensor cores while pass q's warps finish (P / Z MMAs, code tile) and is done
+  // when pass q + 1's softmax starts (r02: phi issue + wait was 2.3 K of 7.8 K cycles per pass)
+  const int npi = npass * (c_hi - c_lo);
+  auto issue_phi = [&](int q) {
+    const int qh = q % npass, qc = q / npass;
+    if (qh == 0) tc::mbar_wait(&sm.ma[0], (uint32_t)qc & 1u);
+    tc::fence_after_sync();
+    ft_gemm(tb + ((q & 1) ? FT_COL_PHI1 : FT_COL_PHI), sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false,
+            qh == 0 ? &sm.ma[1] : nullptr, (uint32_t)qc & 1u, 2);
+    tc::mma_commit_w(&sm.mphi);
+  };
+  if (warp == FT_THREADS / 32 - 1) issue_phi(0);
+  for (int pi = 0; pi < npi; ++pi) {
     const int hp = pi % npass, ic = pi / npass, ci = c_lo + ic, it = pi;
+    const uint32_t col_phi = (pi & 1) ? FT_COL_PHI1 : FT_COL_PHI;
     FT_STAMP(0);
-    if (warp == 0) {  // phi GEMM: Z = k_err W_h (passes hi.hi, hi.lo once A hi has landed, lo.hi after A lo)
-      if (hp == 0) tc::mbar_wait(&sm.ma[0], (uint32_t)ic & 1u);
-      tc::fence_after_sync();
-      ft_gemm(tb + FT_COL_PHI, sm.a, sm.w[0], sm.w[1], FT_IDESC_PHI, false, hp == 0 ? &sm.ma[1] : nullptr,
-              (uint32_t)ic & 1u, 2);
-      tc::mma_commit_w(&sm.mphi);
-    }
     FT_STAMP(1);
     tc::mbar_wait(&sm.mphi, (uint32_t)it & 1u);
     tc::fence_after_sync();
@@ -1364,8 +1373,8 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     {
       const int t = 32 * (warp & 3) + lane;
       float z[64];
-      tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part, reinterpret_cast<uint32_t*>(z));
-      tc::tmem_ld32(lane_addr + FT_COL_PHI + 64 * part + 32, reinterpret_cast<uint32_t*>(z) + 32);
+      tc::tmem_ld32(lane_addr + col_phi + 64 * part, reinterpret_cast<uint32_t*>(z));
+      tc::tmem_ld32(lane_addr + col_phi + 64 * part + 32, reinterpret_cast<uint32_t*>(z) + 32);
       tc::wait_ld();
       FT_STAMP(5);
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 chains (exact: max)
@@ -1420,7 +1429,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
     tc::fence_before_sync();
     __syncthreads();
     FT_STAMP(3);
-    if (warp == 0) {  // S GEMM: D^T += codes^T (s' Phi)
+    if (warp == 0) {  // S GEMM: D^T += codes^T (s' Phi), then the next pass's phi GEMM
       tc::fence_after_sync();
       ft_gemm_s(tb + FT_COL_S + 128 * hp, sm.cv, sm.ps[0], sm.ps[1], ic > 0);
       tc::mma_commit_w(&sm.ms);
@@ -1466,7 +1475,15 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       if (lane == 0) ft_load_c(sm, a, slot0 + ci + 1);
       __syncwarp();
     }
-    __syncthreads();  // the A rows (red) and s' Phi reads are done before the next pass writes them
+    // the A rows (red) and s' Phi reads are done before the next pass writes them.  The last warp
+    // only arrives, then issues the next pass's phi GEMM (its issue stalls while the tensor cores
+    // drain the S GEMM; the next softmax waits for that GEMM anyway)
+    if (warp == FT_THREADS / 32 - 1) {
+      asm volatile("bar.arrive 1, %0;\n" ::"r"(FT_THREADS) : "memory");
+      if (pi + 1 < npi) issue_phi(pi + 1);
+    } else {
+      asm volatile("bar.sync 1, %0;\n" ::"r"(FT_THREADS) : "memory");
+    }
     FT_STAMP(4);
   }
 
@@ -1553,7 +1570,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
   tc::fence_before_sync();
   __syncthreads();
   FT_PHASE(3);
-  if (warp == 0) tc::tmem_dealloc(tb, npass == 2 ? FT_TMEM2 : FT_TMEM);
+  if (warp == 0) tc::tmem_dealloc(tb, FT_TMEM2);
 }
 
 
