@@ -758,7 +758,10 @@ struct QkSmem {
   uint8_t codes[G * D];  // value codes [token][channel] (swizzled, vsw)
   double2 kpar[D];
   float4 kparf[D];
-  uint16_t vt[G / 2][VT_LD];  // a value CTA's ring tokens, token-major (vsplit >= 2)
+  union {
+    uint16_t vt[G / 2][VT_LD];  // a value CTA's ring tokens, token-major (vsplit >= 2)
+    uint16_t vp[G][D];          // a prefill chunk's value rows (cp.async during K1)
+  };
   double dv[FT_THREADS / 32][D];  // per warp: the token of a dense re-evaluation, fp64
 };
 #ifdef KVLC_TRACE
@@ -796,7 +799,8 @@ __device__ long long g_qtok[128][24][2];
 #define KVLC_QK_MINB 3  // 3 CTAs per SM (80 registers, 84 B spills) measured 2 % faster than 2
 #endif
 __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const FlushArgs a, const SeqInfo seq) {
-  __shared__ __align__(16) QkSmem sm;
+  extern __shared__ __align__(16) uint8_t qk_raw[];  // QkSmem (60 KB: dynamic)
+  QkSmem& sm = *reinterpret_cast<QkSmem*>(qk_raw);
   const kvlc_cache& c = a.c;
   const int unit = blockIdx.y, ci = blockIdx.x;
   const int b = unit / c.Hkv;
@@ -824,6 +828,14 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
   };
   const size_t slot = (size_t)unit * a.slot_stride + ci;
   const int zpart = blockIdx.z;
+  // a prefill chunk's value rows (contiguous token rows) are copied into shared memory while K1
+  // runs: K2 then reads its tokens with one 8-B load per lane, no address math or register ring
+  const bool pstaged = a.vsplit == 0 && a.v_c == 1 && (a.v_t & 7) == 0 && (reinterpret_cast<uintptr_t>(V) & 15) == 0;
+  if (pstaged) {
+    for (int i = tid; i < G * D / 8; i += FT_THREADS)
+      tc::cp_async16(&sm.vp[i / (D / 8)][(i % (D / 8)) * 8], V + (size_t)(i / (D / 8)) * a.v_t + (i % (D / 8)) * 8);
+    tc::cp_commit();
+  }
   if (zpart == 0) {
     // ---- K1: keys, channel-wise.  Warp w: channels 16w..16w+15; lane l: tokens 4l..4l+3
     // (16-B vector loads).  Codes in fp32 with the exact fp64 decision near rounding
@@ -951,6 +963,10 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
     const int ntok = a.vsplit ? G / a.vsplit : G;
     const bool staged = a.v_c != 1 && a.v_t == 1 && ntok <= G / 2 && ntok % 8 == 0 &&
                         (reinterpret_cast<uintptr_t>(V) & 15) == 0 && (a.v_c & 7) == 0;
+    if (pstaged) {
+      tc::cp_wait<0>();
+      __syncthreads();
+    }
     if (staged) {
       const int per_row = ntok / 8;
       for (int i = tid; i < D * per_row; i += FT_THREADS) {
@@ -971,12 +987,16 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
 #endif
     // the token loop compiled once per source kind (a runtime `staged` test inside it was
     // if-converted: both load paths issued for every token, ~60 instructions)
+    // source kinds: 0 global (register ring), 1 ring values staged (vt), 2 prefill rows staged (vp)
     auto k2_tokens = [&](auto st_c) {
-      constexpr bool ST = decltype(st_c)::value;
+      constexpr int SRC = decltype(st_c)::value;
+      constexpr bool ST = SRC != 0;
       auto ldvs = [&](int t) -> uint2 {
-        if constexpr (ST) {
+        if constexpr (SRC == 1) {
           const uint32_t* p = reinterpret_cast<const uint32_t*>(&sm.vt[t - t_lo][lane * 4]);
           return make_uint2(p[0], p[1]);
+        } else if constexpr (SRC == 2) {
+          return *reinterpret_cast<const uint2*>(&sm.vp[t][lane * 4]);
         } else {
           return ldv(t);
         }
@@ -1196,9 +1216,11 @@ __global__ void __launch_bounds__(FT_THREADS, KVLC_QK_MINB) quant_kernel(const F
       }
     };
     if (staged)
-      k2_tokens(std::true_type{});
+      k2_tokens(std::integral_constant<int, 1>{});
+    else if (pstaged)
+      k2_tokens(std::integral_constant<int, 2>{});
     else
-      k2_tokens(std::false_type{});
+      k2_tokens(std::integral_constant<int, 0>{});
 #ifdef KVLC_TRACE
     if (lane == 0 && blockIdx.x == 0 && blockIdx.z == 1 && blockIdx.y < 128) {
       g_qtok[blockIdx.y][9 + warp][0] = gtimer();
@@ -1654,7 +1676,8 @@ int launch_tc_flush(const kvlc_cache* c, const kvlc_adapter* ad, FlushArgs a, co
   while (vs > 1 && (long long)units * (1 + vs) > 3LL * sms) vs >>= 1;
   if (vsplit_env >= 0) vs = vsplit_env;
   a.vsplit = (a.ring && max_nf == 1 && vs > 0) ? vs : 0;
-  quant_kernel<<<dim3(max_nf, units, a.vsplit ? 1 + a.vsplit : 1), FT_THREADS, 0, s>>>(a, seq);
+  KVLC_CUDA(cudaFuncSetAttribute(quant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QkSmem)));
+  quant_kernel<<<dim3(max_nf, units, a.vsplit ? 1 + a.vsplit : 1), FT_THREADS, sizeof(QkSmem), s>>>(a, seq);
   if ((rc = check_launch("quant"))) return rc;
   KVLC_CUDA(cudaFuncSetAttribute(flush_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FtSmem)));
   // one chunk per unit (decode-time ring flush): both feature halves in one CTA
