@@ -956,7 +956,13 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
 
 // 55 KB of dynamic shared memory per CTA: 4 CTAs per SM for groups of <= 4 heads (q in
 // shared memory, 128 registers), 3 for larger groups (q and the lo B parts in registers)
-constexpr int wpc_minb(int ng) { return ng <= 4 ? 4 : 3; }
+// CTAs per SM of the warp-per-chunk kernel for groups of <= 4 heads: 3 (162 registers) measured
+// faster than 4 (the 128-register cap) and 2: config 2 kernel pair 36.4 -> 34.7 us (2: 42.3),
+// config 4 28.9 -> 28.6, config 1 8.6 -> 8.4 (tools/run_abvar.sh, r02)
+#ifndef KVLC_WPC_MINB4
+#define KVLC_WPC_MINB4 3
+#endif
+constexpr int wpc_minb(int ng) { return ng <= 4 ? KVLC_WPC_MINB4 : 3; }
 template <int NG, int EXTRA>
 __global__ void __launch_bounds__(THREADS, wpc_minb(NG)) split_kernel_wpc(const DecArgs a) {
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -1217,7 +1223,14 @@ int plan_for(const kvlc_cache* c, const kvlc_decode_opts* o, int chunk_lo, int c
     const long long warps = 148LL * wpc_minb(p.NG) * WARPS;
     const long long chunks = (long long)p.U * std::max(span, 1);
     // chunks per warp; multi-wave workloads keep splits short (the tail of the last wave)
-    long long cpw = std::min(6LL, std::max(2LL, (chunks + warps / 2) / warps));
+    // at most 6 chunks per warp, 4 for groups above 4 heads (their chunk costs more: Qwen B16 x 32k
+    // 72.2 -> 67.1 us; Llama B64 x 8k prefers 6: 115.3 vs 117.9).  KVLC_CPWCAP overrides (A/B)
+    static const int cpw_env = [] {
+      const char* e = getenv("KVLC_CPWCAP");
+      return e ? atoi(e) : 0;
+    }();
+    const long long cpw_cap = cpw_env ? cpw_env : (p.NG > 4 ? 4 : 6);
+    long long cpw = std::min(cpw_cap, std::max(2LL, (chunks + warps / 2) / warps));
     long long nsq = (std::max(span, 1) + 4 * cpw - 1) / (4 * cpw);
     static const int rec_cap = [] {
       const char* e = getenv("KVLC_RECCAP");

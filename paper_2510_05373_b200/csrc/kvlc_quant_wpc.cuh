@@ -287,7 +287,12 @@ __device__ __forceinline__ void run_quant_wpc(const DecArgs& a, int unit, int sp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   constexpr bool HILO = NG <= 4;
-  constexpr bool QSM = HILO;  // q from shared memory (register budget of 4 CTAs per SM)
+#ifndef KVLC_WPC_QSM
+#define KVLC_WPC_QSM 1
+#endif
+  // q from shared memory: frees registers for the pipeline (also at 3 CTAs per SM: 34.7 vs 35.0 us
+  // with q in registers, config 2)
+  constexpr bool QSM = HILO && KVLC_WPC_QSM;
   WarpState<NG> st;
   st.init();
   const int lo = a.chunk_lo + split * a.cpc;
