@@ -962,7 +962,10 @@ __global__ void __launch_bounds__(THREADS, KVLC_SPLIT_MINB) split_kernel(const D
 #ifndef KVLC_WPC_MINB4
 #define KVLC_WPC_MINB4 3
 #endif
-constexpr int wpc_minb(int ng) { return ng <= 4 ? KVLC_WPC_MINB4 : 3; }
+#ifndef KVLC_WPC_MINB8
+#define KVLC_WPC_MINB8 3  // the same for groups of 5-8 heads
+#endif
+constexpr int wpc_minb(int ng) { return ng <= 4 ? KVLC_WPC_MINB4 : KVLC_WPC_MINB8; }
 template <int NG, int EXTRA>
 __global__ void __launch_bounds__(THREADS, wpc_minb(NG)) split_kernel_wpc(const DecArgs a) {
   extern __shared__ __align__(128) unsigned char dsm[];
