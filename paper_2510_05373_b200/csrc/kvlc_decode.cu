@@ -1334,8 +1334,11 @@ int launch_ng(const kvlc_cache* c, const kvlc_adapter* ad, const uint16_t* q, co
     const char* e = getenv("KVLC_CORRSPLIT");
     return e ? atoi(e) : 0;
   }();
+  // r02 late (3 warp-per-chunk CTAs per SM): groups of <= 4 heads take the halves in every grid,
+  // one wave included (B1 x 4k, 8 kv heads x 4 heads: 10.70 -> 8.48 us; B1 x 1k x 8 MHA heads
+  // 8.25 -> 7.72; B4 x 4k 13.97 -> 11.67; B1 x 32k 14.62 -> 13.29)
   a.corr_split = corr_split_env ? corr_split_env
-                                : ((long long)p.U * (p.nsq + 1) > 148LL * split_minb(NG, p.wpc) ? 2 : 1);
+                                : ((NG <= 4 || (long long)p.U * (p.nsq + 1) > 148LL * split_minb(NG, p.wpc)) ? 2 : 1);
   // tail tasks: correction half h + residual half h in one CTA (one start-up and q staging
   // instead of two; both are latency-bound) when the correction runs in halves
   static const int tailfuse_env = [] {
