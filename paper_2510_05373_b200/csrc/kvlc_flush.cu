@@ -678,6 +678,21 @@ __device__ __forceinline__ void ft_mma16816(float (&c)[4], uint32_t a0, uint32_t
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+// 2^x for x <= 0 on the FMA pipe (round-to-nearest integer split, degree-6 Taylor of 2^f on
+// |f| <= 1/2: ~1.2e-7 relative, like ex2.approx; x < -125 gives ~2^-125 instead of ex2.ftz's 0)
+__device__ __forceinline__ float ft_exp2_fma(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: the integer part in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  float p = 1.5403530e-4f;
+  p = fmaf(p, f, 1.3333558e-3f);
+  p = fmaf(p, f, 9.6181291e-3f);
+  p = fmaf(p, f, 5.5504109e-2f);
+  p = fmaf(p, f, 2.4022651e-1f);
+  p = fmaf(p, f, 6.9314718e-1f);
+  p = fmaf(p, f, 1.f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
 // ft_hilo of two values with packed conversions (the same bits: each half is rounded to nearest)
 __device__ __forceinline__ void ft_hilo2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
   const __half2 h = __floats2half2_rn(x0, x1);
@@ -1410,8 +1425,13 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
       float s4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 partial sums: a 64-deep add chain was latency
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
+        // 3 of every 8 on the FMA pipe: the MUFU (16 ex2 per clock per SM) bounded this loop
         float e2;
-        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(fmaf(z[i], 1.4426950408889634f, -m)));
+        const float xe = fmaf(z[i], 1.4426950408889634f, -m);
+        if ((i & 7) < 3)
+          e2 = ft_exp2_fma(xe);
+        else
+          asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(xe));
         z[i] = e2;
         s4[i & 3] += e2;
       }
