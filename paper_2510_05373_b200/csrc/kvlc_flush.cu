@@ -678,6 +678,9 @@ __device__ __forceinline__ void ft_mma16816(float (&c)[4], uint32_t a0, uint32_t
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+#ifndef KVLC_EXP_FMA
+#define KVLC_EXP_FMA 3  // of every 8 softmax exponentials on the FMA pipe
+#endif
 // 2^x for x <= 0 on the FMA pipe (round-to-nearest integer split, degree-6 Taylor of 2^f on
 // |f| <= 1/2: ~1.2e-7 relative, like ex2.approx; x < -125 gives ~2^-125 instead of ex2.ftz's 0)
 __device__ __forceinline__ float ft_exp2_fma(float x) {
@@ -1428,7 +1431,7 @@ __global__ void __launch_bounds__(FT_THREADS, 1) flush_tc_kernel(const FlushArgs
         // 3 of every 8 on the FMA pipe: the MUFU (16 ex2 per clock per SM) bounded this loop
         float e2;
         const float xe = fmaf(z[i], 1.4426950408889634f, -m);
-        if ((i & 7) < 3)
+        if ((i & 7) < KVLC_EXP_FMA)
           e2 = ft_exp2_fma(xe);
         else
           asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e2) : "f"(xe));
